@@ -1,0 +1,45 @@
+// Bond kernel job description (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include "ttp_common.cuh"
+
+#define BOND_THREADS 512
+
+struct BondJob {
+  int m, r;               // tall block rows / cols (m >= r)
+  long long mat_stride;   // complex elements per instance for A, W, B
+  cplx* A;                // sampled block (col-major, ld m); overwritten by Q
+  cplx* W;                // working copy
+  cplx* B;                // maxvol matrix
+  int* iwork;             // 2m ints per instance
+  long long iw_stride;
+  double* dwork;          // 2m doubles per instance
+  long long dw_stride;
+  const int* active;      // optional per-instance mask
+  int* status;            // per-instance ttp_status (skips instances != OK)
+  int* err_bond;          // optional: bond index recorded with an error
+  int bond;               // bond number of this launch (SingularMatrixError.bond)
+  double rank_tol;        // 0 on the cross path (cross.py:343), 1e-12 for maxvol()
+  long long max_iters;    // < 0: None  (10 * m)
+  double slack;
+  int pairwise;           // allow _pairwise_refine (m <= 96, r <= 8)
+  int* sel_out;           // optional: sorted selection per instance
+  long long sel_stride;
+  // factor output (write_mode 0: none, 1: left-to-right core, 2: right-to-left core)
+  int write_mode;
+  cplx* core_out;         // core base (already offset to this site)
+  long long core_stride;  // complex elements per instance
+  // nested index-set update
+  int* set_out;           // destination set base (all instances)
+  const int* set_in;      // parent set base
+  long long set_stride;   // ints per instance
+  long long set_out_off, set_in_off;
+  int set_d;              // row stride of the packed sets (= d)
+  int klen;               // tuple length of the new set
+  int na;                 // axis size (left-to-right decode)
+  int rr;                 // right count (right-to-left decode)
+};
+
+size_t bond_smem_bytes(int r);
+cudaError_t launch_bond(const BondJob& job, int n_inst, cudaStream_t s);

@@ -1,0 +1,297 @@
+// K6 / K7: tensor-train contractions.
+//
+//  * tt_inner (tensor_train.py:143-159): per site the environment (Db x Dk)
+//    is pushed through  env' = sum_s conj(B_s)^T (env K_s).  One CTA per
+//    instance; env and the (env K_s) tile live in shared memory, each thread
+//    owns a fixed set of env' accumulators in registers, and the s-sum runs
+//    in order, so the result is bitwise reproducible.
+//  * tt_evaluate_many (tensor_train.py:126-140):
+//      - eval_warp_kernel: one warp per sample (public API, any index set);
+//      - site_group_kernel: the convergence-check path.  The 50 000 samples
+//        of tt_rand_sample_diff are fixed per (seed, shape)
+//        (tensor_train.py:191-194), so they are bucketed once per site by
+//        their index there; a CTA then loads the single core slice
+//        G_k[:, s, :] into shared memory and streams every sample of bucket
+//        s through it.  Each slice is read from HBM once per sweep instead
+//        of once per sample.
+#include "ttp_internal.h"
+
+namespace {
+
+// ----------------------------------------------------------------- tt_inner
+struct TTDev {
+  const cplx* cores;
+  long long stride;
+  long long off[TTP_MAX_D + 1];
+  int bonds[TTP_MAX_D + 1];
+  int shape[TTP_MAX_D];
+  int d;
+};
+
+TTDev tt_dev(const ttp_tt_batch& b) {
+  TTDev t;
+  t.cores = reinterpret_cast<const cplx*>(b.d_cores);
+  t.stride = b.stride;
+  t.d = b.d;
+  for (int k = 0; k <= b.d; ++k) {
+    t.off[k] = b.h_offsets[k];
+    t.bonds[k] = b.h_bonds[k];
+  }
+  for (int k = 0; k < b.d; ++k) t.shape[k] = b.h_shape[k];
+  return t;
+}
+
+constexpr int INNER_THREADS = 256;
+constexpr int INNER_ACC = 16;  // (64*64)/256 accumulators per thread max
+
+__global__ void __launch_bounds__(INNER_THREADS)
+tt_inner_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) {
+  extern __shared__ cplx sm[];
+  const int inst = blockIdx.x;
+  const int tid = threadIdx.x;
+  int maxb = 1, maxk = 1;
+  for (int k = 0; k <= bra.d; ++k) {
+    maxb = max(maxb, bra.bonds[k]);
+    maxk = max(maxk, ket.bonds[k]);
+  }
+  cplx* env = sm;                 // Db x Dk
+  cplx* tmp = sm + maxb * maxk;   // Db x Dk'
+  if (tid == 0) env[0] = mk(1.0, 0.0);
+  __syncthreads();
+  for (int k = 0; k < bra.d; ++k) {
+    const int Db = bra.bonds[k], Db2 = bra.bonds[k + 1];
+    const int Dk = ket.bonds[k], Dk2 = ket.bonds[k + 1];
+    const int n = bra.shape[k];
+    const cplx* B = bra.cores + inst * bra.stride + bra.off[k];
+    const cplx* K = ket.cores + inst * ket.stride + ket.off[k];
+    const int nacc = Db2 * Dk2;
+    cplx acc[INNER_ACC];
+#pragma unroll
+    for (int q = 0; q < INNER_ACC; ++q) acc[q] = mk(0.0, 0.0);
+    for (int s = 0; s < n; ++s) {
+      // tmp[a, c] = sum_b env[a, b] * K[b, s, c]
+      for (int e = tid; e < Db * Dk2; e += INNER_THREADS) {
+        const int a = e / Dk2, c = e - a * Dk2;
+        cplx t = mk(0.0, 0.0);
+        for (int b = 0; b < Dk; ++b) t = cfma(env[a * Dk + b], K[((long long)b * n + s) * Dk2 + c], t);
+        tmp[e] = t;
+      }
+      __syncthreads();
+      // env'[a2, c] += sum_a conj(B[a, s, a2]) * tmp[a, c]
+#pragma unroll
+      for (int q = 0; q < INNER_ACC; ++q) {
+        const int e = tid + q * INNER_THREADS;
+        if (e < nacc) {
+          const int a2 = e / Dk2, c = e - a2 * Dk2;
+          cplx t = acc[q];
+          for (int a = 0; a < Db; ++a)
+            t = cfmac(B[((long long)a * n + s) * Db2 + a2], tmp[a * Dk2 + c], t);
+          acc[q] = t;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < INNER_ACC; ++q) {
+      const int e = tid + q * INNER_THREADS;
+      if (e < nacc) env[e] = acc[q];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) out[inst] = env[0];
+}
+
+// ------------------------------------------------------- tt_evaluate_many
+constexpr int EVAL_WARPS = 8;
+
+__global__ void __launch_bounds__(EVAL_WARPS * 32)
+eval_warp_kernel(const TTDev tt, const int* __restrict__ idx, long long m, cplx* __restrict__ out) {
+  const int inst = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const long long j = (long long)blockIdx.x * EVAL_WARPS + (threadIdx.x >> 5);
+  if (j >= m) return;
+  const cplx* base = tt.cores + inst * tt.stride;
+  // lane owns vec entries lane and lane+32 (bond dims <= 64)
+  cplx v0 = mk(0.0, 0.0), v1 = mk(0.0, 0.0);
+  {
+    const int r1 = tt.bonds[1];
+    const int i0 = idx[j * tt.d];
+    const cplx* c0 = base + tt.off[0] + (long long)i0 * r1;
+    if (lane < r1) v0 = c0[lane];
+    if (lane + 32 < r1) v1 = c0[lane + 32];
+  }
+  for (int k = 1; k < tt.d; ++k) {
+    const int ra = tt.bonds[k], rb = tt.bonds[k + 1], n = tt.shape[k];
+    const int ik = idx[j * tt.d + k];
+    const cplx* G = base + tt.off[k];
+    cplx w0 = mk(0.0, 0.0), w1 = mk(0.0, 0.0);
+    for (int a = 0; a < ra; ++a) {
+      const cplx src = (a < 32) ? v0 : v1;
+      cplx va;
+      va.x = __shfl_sync(0xffffffffu, src.x, a & 31);
+      va.y = __shfl_sync(0xffffffffu, src.y, a & 31);
+      const cplx* row = G + ((long long)a * n + ik) * rb;
+      if (lane < rb) w0 = cfma(va, row[lane], w0);
+      if (lane + 32 < rb) w1 = cfma(va, row[lane + 32], w1);
+    }
+    v0 = w0;
+    v1 = w1;
+  }
+  if (lane == 0) out[inst * m + j] = v0;
+}
+
+}  // namespace
+
+// Site-0 gather and grouped site kernels for the convergence check (used by
+// the cross driver).
+__global__ void conv_site0_kernel(const cplx* __restrict__ cores, long long stride, long long off0,
+                                  int r1, const int* __restrict__ idx, int d, long long m,
+                                  cplx* __restrict__ V, long long vstride,
+                                  const int* __restrict__ active) {
+  const int inst = blockIdx.y;
+  if (active && !active[inst]) return;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * r1) return;
+  const long long j = e / r1;
+  const int c = (int)(e - j * r1);
+  V[inst * vstride + e] = cores[inst * stride + off0 + (long long)idx[j * d] * r1 + c];
+}
+
+__global__ void conv_site_kernel(const cplx* __restrict__ cores, long long stride, long long offk,
+                                 int ra, int n, int rb, const int* __restrict__ perm,
+                                 const int* __restrict__ goff, const cplx* __restrict__ Vin,
+                                 cplx* __restrict__ Vout, long long vstride,
+                                 const int* __restrict__ active) {
+  extern __shared__ cplx G[];  // ra x rb slice
+  const int inst = blockIdx.y;
+  if (active && !active[inst]) return;
+  const int s = blockIdx.x;
+  const cplx* src = cores + inst * stride + offk;
+  for (int e = threadIdx.x; e < ra * rb; e += blockDim.x) {
+    const int a = e / rb, c = e - a * rb;
+    G[e] = src[((long long)a * n + s) * rb + c];
+  }
+  __syncthreads();
+  const int g0 = goff[s], g1 = goff[s + 1];
+  const int per = blockDim.x / rb;  // samples per pass
+  const int sub = threadIdx.x / rb, c = threadIdx.x - sub * rb;
+  if (sub >= per) return;
+  const cplx* vin = Vin + inst * vstride;
+  cplx* vout = Vout + inst * vstride;
+  for (int t = g0 + sub; t < g1; t += per) {
+    const long long j = perm[t];
+    const cplx* row = vin + j * ra;
+    cplx acc = mk(0.0, 0.0);
+    for (int a = 0; a < ra; ++a) acc = cfma(row[a], G[a * rb + c], acc);
+    vout[j * rb + c] = acc;
+  }
+}
+
+// Fixed-order per-instance sums of |exact - approx| and |exact|.
+__global__ void sample_diff_kernel(const cplx* __restrict__ exact, const cplx* __restrict__ approx,
+                                   long long m, long long estride, long long astride,
+                                   double* __restrict__ out, const int* __restrict__ active) {
+  const int inst = blockIdx.x;
+  if (active && !active[inst]) return;
+  __shared__ double sn[32], sd[32];
+  double num = 0.0, den = 0.0;
+  const cplx* ex = exact + inst * estride;
+  const cplx* ap = approx + inst * astride;
+  for (long long j = threadIdx.x; j < m; j += blockDim.x) {
+    const cplx e = ex[j];
+    num += cabsh(csub(e, ap[j]));
+    den += cabsh(e);
+  }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sn[w] = num;
+    sd[w] = den;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    num = lane < nw ? sn[lane] : 0.0;
+    den = lane < nw ? sd[lane] : 0.0;
+    num = warp_sum(num);
+    den = warp_sum(den);
+    if (lane == 0) {
+      out[2 * inst] = num;
+      out[2 * inst + 1] = den;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- C ABI
+static bool tt_shape_ok(const ttp_tt_batch* t) {
+  if (!t || t->d < 1 || t->d > TTP_MAX_D || t->n_inst < 0) return false;
+  for (int k = 0; k <= t->d; ++k)
+    if (t->h_bonds[k] < 1 || t->h_bonds[k] > 64) return false;
+  return t->h_bonds[0] == 1 && t->h_bonds[t->d] == 1;
+}
+
+extern "C" int ttp_tt_inner(const ttp_tt_batch* bra, const ttp_tt_batch* ket, double* d_out,
+                            void* stream) {
+  if (!tt_shape_ok(bra) || !tt_shape_ok(ket) || bra->d != ket->d || bra->n_inst != ket->n_inst)
+    return ttp_fail(TTP_ERR_INVALID, "tt_inner: bad train batch");
+  for (int k = 0; k < bra->d; ++k)
+    if (bra->h_shape[k] != ket->h_shape[k])
+      return ttp_fail(TTP_ERR_INVALID, "tt_inner: physical shape mismatch");
+  if (bra->n_inst == 0) return TTP_OK;
+  TTDev b = tt_dev(*bra), k = tt_dev(*ket);
+  int maxb = 1, maxk = 1;
+  for (int q = 0; q <= bra->d; ++q) {
+    maxb = max(maxb, bra->h_bonds[q]);
+    maxk = max(maxk, ket->h_bonds[q]);
+  }
+  const size_t smem = sizeof(cplx) * (size_t)(2 * maxb * maxk);
+  TTP_CUDA_CHECK(cudaFuncSetAttribute(tt_inner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  tt_inner_kernel<<<bra->n_inst, INNER_THREADS, smem, (cudaStream_t)stream>>>(
+      b, k, reinterpret_cast<cplx*>(d_out));
+  TTP_CUDA_CHECK(cudaGetLastError());
+  return TTP_OK;
+}
+
+extern "C" size_t ttp_tt_eval_workspace(const ttp_tt_batch*, int64_t) { return 0; }
+
+extern "C" int ttp_tt_eval(const ttp_tt_batch* tt, const int32_t* d_idx, int64_t m, double* d_out,
+                           void*, size_t, void* stream) {
+  if (!tt_shape_ok(tt) || m < 0) return ttp_fail(TTP_ERR_INVALID, "tt_eval: bad train batch");
+  if (m == 0 || tt->n_inst == 0) return TTP_OK;
+  TTDev t = tt_dev(*tt);
+  dim3 grid((unsigned)((m + EVAL_WARPS - 1) / EVAL_WARPS), (unsigned)tt->n_inst);
+  eval_warp_kernel<<<grid, EVAL_WARPS * 32, 0, (cudaStream_t)stream>>>(
+      t, d_idx, m, reinterpret_cast<cplx*>(d_out));
+  TTP_CUDA_CHECK(cudaGetLastError());
+  return TTP_OK;
+}
+
+extern "C" int ttp_sample_diff(int32_t n_inst, int64_t m, const double* d_exact,
+                               const double* d_approx, double* h_out, void* d_ws, size_t ws_bytes,
+                               void* stream) {
+  if (n_inst < 0 || m < 1) return ttp_fail(TTP_ERR_INVALID, "sample count must be >= 1");
+  if (ws_bytes < sizeof(double) * 2 * (size_t)n_inst)
+    return ttp_fail(TTP_ERR_WORKSPACE, "sample_diff: workspace too small");
+  if (n_inst == 0) return TTP_OK;
+  double* sums = reinterpret_cast<double*>(d_ws);
+  sample_diff_kernel<<<n_inst, 1024, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const cplx*>(d_exact), reinterpret_cast<const cplx*>(d_approx), m, m, m,
+      sums, nullptr);
+  TTP_CUDA_CHECK(cudaGetLastError());
+  std::string err;
+  double* host = new double[2 * (size_t)n_inst];
+  cudaError_t e = cudaMemcpyAsync(host, sums, sizeof(double) * 2 * n_inst, cudaMemcpyDeviceToHost,
+                                  (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    delete[] host;
+    return ttp_record_cuda_error(e);
+  }
+  for (int i = 0; i < n_inst; ++i) {
+    const double num = host[2 * i], den = host[2 * i + 1];
+    h_out[i] = (den == 0.0) ? (num == 0.0 ? 0.0 : INFINITY) : num / den;
+  }
+  delete[] host;
+  return TTP_OK;
+}

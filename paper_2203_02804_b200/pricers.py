@@ -1,0 +1,230 @@
+"""Fourier pricing engines on the GPU (reference pricers.py).
+
+``price_fourier_tt`` is the drop-in boundary of the hot path
+(pricers.py:256-294): two device TT-crosses (phi and conj(vhat)) followed by
+the device tt_inner.  ``price_fourier_tt_batch`` prices many independent
+options per call -- the throughput path the benchmark measures -- and keeps
+the trains resident on the GPU between the crosses and the contraction.
+``price_fourier_dense`` is the full-grid cross-check (pricers.py:199-231,
+kernel K8).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .cross import CrossConfig, tt_cross_batch
+from .errors import CapacityError, ResidueError, StripConditionError
+from .oracles import OracleBatch, PayoffGridOracle, PhiGridOracle
+from .tensor_train import tt_inner_batch
+
+__all__ = [
+    "GridSpec",
+    "PricingResult",
+    "grid_admissible",
+    "table1_hyperparams",
+    "phi_grid_oracle",
+    "payoff_grid_oracle",
+    "price_fourier_dense",
+    "price_fourier_dense_batch",
+    "price_fourier_tt",
+    "price_fourier_tt_batch",
+    "DENSE_TERM_CAP",
+]
+
+DENSE_TERM_CAP = 100_000_000
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Per-axis grid of n+1 points j = -n/2..n/2 (pricers.py:49-86)."""
+
+    n: int
+    eta: float
+    alpha: float
+    d: int
+
+    def __post_init__(self):
+        if self.n < 2 or self.n % 2 != 0:
+            raise ValueError(f"n must be even and >= 2, got {self.n}")
+        if self.eta <= 0:
+            raise ValueError("eta must be > 0")
+        if self.d < 1:
+            raise ValueError("d must be >= 1")
+
+    @property
+    def points_per_axis(self):
+        return self.n + 1
+
+    @property
+    def n_terms(self):
+        return (self.n + 1) ** self.d
+
+    def index_to_u(self, j):
+        return self.eta * np.asarray(j)
+
+    def contour(self, idx):
+        return self.eta * (np.asarray(idx, dtype=np.int64) - self.n // 2) + 1j * self.alpha
+
+
+@dataclass
+class PricingResult:
+    price: float
+    method: str
+    wall_time_s: float
+    diagnostics: dict = field(default_factory=dict)
+
+    def to_dict(self, include_timing=True):
+        diag = {k: (v.to_dict() if hasattr(v, "to_dict") else v) for k, v in self.diagnostics.items()}
+        out = {"price": self.price, "method": self.method, "diagnostics": diag}
+        if include_timing:
+            out["wall_time_s"] = self.wall_time_s
+        return out
+
+
+def grid_admissible(grid, payoff="min"):
+    """Strip conditions of the payoff transform (pricers.py:108-127)."""
+    reasons = []
+    if payoff == "min":
+        if grid.alpha <= 0:
+            reasons.append(f"imaginary shift {grid.alpha} is not positive")
+        if grid.d * grid.alpha <= 1:
+            reasons.append(f"sum of shifts d*alpha = {grid.d * grid.alpha} is not above 1")
+    elif payoff == "call":
+        if grid.alpha <= 1:
+            reasons.append(f"imaginary shift {grid.alpha} is not above 1")
+    else:
+        raise ValueError(f"unknown payoff kind {payoff!r}")
+    return not reasons, reasons
+
+
+def _require_admissible(grid):
+    ok, reasons = grid_admissible(grid, "min")
+    if not ok:
+        raise StripConditionError("; ".join(reasons))
+
+
+_TABLE1 = {2: (0.5, 20, 10), 3: (0.4, 20, 10), 4: (0.3, 30, 15), 5: (0.3, 30, 15),
+           6: (0.2, 30, 15), 7: (0.2, 40, 20), 8: (0.2, 40, 20), 9: (0.2, 40, 20),
+           10: (0.2, 40, 20)}
+
+
+def table1_hyperparams(d):
+    """(eta, bond_v, bond_phi) of the paper's Table I (pricers.py:136-151)."""
+    if d < 2:
+        raise ValueError("tabulated hyperparameters start at d=2")
+    return _TABLE1.get(d, (0.2, 50, 25))
+
+
+def phi_grid_oracle(model, grid):
+    return PhiGridOracle(model, grid)
+
+
+def payoff_grid_oracle(model, grid):
+    return PayoffGridOracle(model, grid, conj=True)
+
+
+def _prefactor(model, grid, t):
+    return np.exp(-model.r * (model.T - t)) * grid.eta ** grid.d / (2.0 * np.pi) ** grid.d
+
+
+def price_fourier_dense_batch(models, grid, t=0.0, term_cap=DENSE_TERM_CAP):
+    """Dense contour sums for several models on one grid -> list of PricingResult."""
+    for m in models:
+        if m.d != grid.d:
+            raise ValueError(f"model has d={m.d} but grid has d={grid.d}")
+    _require_admissible(grid)
+    if grid.n_terms > term_cap:
+        raise CapacityError(f"dense sum needs {grid.n_terms} terms, cap is {term_cap}")
+    torch = _lib.require_device()
+    lib = _lib.load_library()
+    start = time.perf_counter()
+    phi = OracleBatch([PhiGridOracle(m, grid) for m in models])
+    vhat = OracleBatch([PayoffGridOracle(m, grid, conj=False) for m in models])
+    shape = np.full(grid.d, grid.points_per_axis, dtype=np.int32)
+    d_shape = torch.from_numpy(shape).to("cuda")
+    n = len(models)
+    ws_bytes = lib.ttp_dense_workspace(n, grid.n_terms)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    sums = (ctypes.c_double * (2 * n))()
+    st = lib.ttp_dense_sum(ctypes.byref(phi.struct), ctypes.byref(vhat.struct),
+                           shape.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                           ctypes.c_void_p(d_shape.data_ptr()), n, sums,
+                           ctypes.c_void_p(ws.data_ptr()), ws_bytes, _lib.stream_handle())
+    _lib.raise_for(st, "dense sum")
+    wall = time.perf_counter() - start
+    out = []
+    for i, m in enumerate(models):
+        acc = complex(sums[2 * i], sums[2 * i + 1])
+        value = _prefactor(m, grid, t) * acc
+        residue = float(abs(value.imag) / abs(value)) if value != 0 else 0.0
+        if residue > 1e-8 and abs(value.imag) > 1e-12:
+            raise ResidueError(f"imaginary residue {residue:.3e} of the contour sum exceeds 1e-8")
+        out.append(PricingResult(float(value.real), "fourier_dense", wall / n,
+                                 {"n_terms": grid.n_terms, "imag_residue": residue}))
+    return out
+
+
+def price_fourier_dense(model, grid, t=0.0, term_cap=DENSE_TERM_CAP):
+    """Dense nested contour sum on the GPU (pricers.py:199-231)."""
+    if model.d != grid.d:
+        raise ValueError(f"model has d={model.d} but grid has d={grid.d}")
+    return price_fourier_dense_batch([model], grid, t=t, term_cap=term_cap)[0]
+
+
+def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference="never",
+                           term_cap=DENSE_TERM_CAP, raise_errors=True):
+    """Price many independent options on one grid with the device TT path.
+
+    All instances share the grid and the two CrossConfigs (so they share the
+    seeded pivot initialisation and convergence samples); parameters differ
+    per instance.  Returns a list of PricingResult (or exceptions when
+    ``raise_errors`` is False).
+    """
+    for m in models:
+        if m.d != grid.d:
+            raise ValueError(f"model has d={m.d} but grid has d={grid.d}")
+    _require_admissible(grid)
+    start = time.perf_counter()
+    shape = (grid.points_per_axis,) * grid.d
+    phi_res = tt_cross_batch([PhiGridOracle(m, grid) for m in models], shape, cfg_phi)
+    v_res = tt_cross_batch([PayoffGridOracle(m, grid, conj=True) for m in models], shape, cfg_v)
+    raw = tt_inner_batch(v_res.trains, phi_res.trains)
+    wall = time.perf_counter() - start
+    results = []
+    dense = None
+    if dense_reference == "auto" and grid.n_terms <= term_cap:
+        dense = price_fourier_dense_batch(models, grid, t=t, term_cap=term_cap)
+    for i, m in enumerate(models):
+        err = phi_res.error_for(i) or v_res.error_for(i)
+        if err is not None:
+            if raise_errors:
+                raise err
+            results.append(err)
+            continue
+        value = _prefactor(m, grid, t) * raw[i]
+        diag = {
+            "cross_phi": phi_res.reports[i],
+            "cross_v": v_res.reports[i],
+            "imag_part": float(value.imag),
+            "oracle_calls_total": phi_res.reports[i].oracle_calls + v_res.reports[i].oracle_calls,
+        }
+        if dense is not None:
+            diag["dense_price"] = dense[i].price
+            diag["eps_trunc"] = float(abs(value.real - dense[i].price) / abs(dense[i].price))
+        results.append(PricingResult(float(value.real), "fourier_tt", wall / len(models), diag))
+    return results
+
+
+def price_fourier_tt(model, grid, cfg_phi, cfg_v, t=0.0, dense_reference="auto",
+                     term_cap=DENSE_TERM_CAP):
+    """Tensor-train contraction of the contour sum (pricers.py:256-294)."""
+    if model.d != grid.d:
+        raise ValueError(f"model has d={model.d} but grid has d={grid.d}")
+    return price_fourier_tt_batch([model], grid, cfg_phi, cfg_v, t=t,
+                                  dense_reference=dense_reference, term_cap=term_cap)[0]
