@@ -1,0 +1,65 @@
+"""Instance-level data parallelism across the GPUs of one box.
+
+Options are independent, so a batch is sharded into contiguous instance
+ranges (rank g gets [g*B/W, (g+1)*B/W)); each rank runs its
+own batched TT-cross and there is no collective on the data path.  The only
+exchange is one all-gather of a fixed-size per-option record at the end
+(NCCL over NVLink on GPUs, gloo in the CPU tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+RECORD_FIELDS = ("price", "imag", "status", "sweeps_phi", "sweeps_v", "calls_phi",
+                 "calls_v", "diff_phi", "diff_v")
+
+
+def shard_range(n_total, rank, world):
+    """Contiguous [lo, hi) slice of ``n_total`` instances owned by ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    lo = (rank * n_total) // world
+    hi = ((rank + 1) * n_total) // world
+    return lo, hi
+
+
+def results_to_records(results):
+    """PricingResult list (or exceptions) -> (n, len(RECORD_FIELDS)) float64."""
+    out = np.full((len(results), len(RECORD_FIELDS)), np.nan)
+    for i, res in enumerate(results):
+        if isinstance(res, Exception):
+            out[i, 2] = 1.0
+            continue
+        cp, cv = res.diagnostics["cross_phi"], res.diagnostics["cross_v"]
+        out[i] = (res.price, res.diagnostics["imag_part"], 0.0, cp.sweeps_used, cv.sweeps_used,
+                  cp.oracle_calls, cv.oracle_calls, cp.final_diff, cv.final_diff)
+    return out
+
+
+def gather_records(local, n_total, device=None):
+    """All-gather per-rank record blocks into the full (n_total, F) array.
+
+    Uses torch.distributed with the process group already initialised
+    (``nccl`` with CUDA tensors, ``gloo`` with CPU tensors).
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    width = local.shape[1]
+    cap = max(shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0] for r in range(world))
+    buf = np.zeros((cap, width))
+    buf[: len(local)] = local
+    t = torch.from_numpy(buf)
+    if device is not None:
+        t = t.to(device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    rows = []
+    for r in range(world):
+        lo, hi = shard_range(n_total, r, world)
+        rows.append(parts[r].cpu().numpy()[: hi - lo])
+    del rank
+    return np.concatenate(rows, axis=0)

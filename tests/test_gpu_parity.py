@@ -1,0 +1,371 @@
+"""GPU parity tests: the CUDA path vs the reference (golden fixtures) and the
+pinned CPU oracle, following the parity ladder of SURVEY.md 8(c).
+
+  P0  evaluators (K1/K2)          <= 1e-12 relative (2e-12 at d=20)
+  P1  contractions (K6/K7)        <= 1e-12 relative
+  P2  dense contour sum (K8)      <= 1e-10 relative
+  P3  decisions (K3-K5)           identical pivot sets / maxvol selections
+  P4  end to end                  within the reference's own reproducibility
+                                  band, and as close to the dense sum as the
+                                  reference is
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import BENCH, load_npz, sets_as_lists, uniform_bonds, unflat_cores
+from oracle import ttp_oracle as O
+import paper_2203_02804_b200 as P
+from paper_2203_02804_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+def tt_of(flat, phys, bonds):
+    return P.TensorTrain(unflat_cores(flat, phys, bonds))
+
+
+def plus_model(d, beta=0.5):
+    return P.MarketModel.with_plus_correlation(d=d, beta=beta, **BENCH)
+
+
+def bench_grid(d, n=50):
+    if d == 1:
+        return P.GridSpec(n=n, eta=0.5, alpha=3.0, d=1)
+    return P.GridSpec(n=n, eta=P.table1_hyperparams(d)[0], alpha=5.0 / d, d=d)
+
+
+# ------------------------------------------------------------------- P0
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_p0_evaluators_match_reference(cid):
+    ev = load_npz("evaluators.npz")
+    m = configs.make_model(cid)
+    g = configs.CONFIGS[cid].grid
+    idx = ev[f"c{cid}_idx"]
+    tol = 2e-12 if cid == 5 else 1e-12
+    assert rel(P.PhiGridOracle(m, g)(idx), ev[f"c{cid}_phi"]) <= tol
+    assert rel(P.PayoffGridOracle(m, g)(idx), ev[f"c{cid}_vhat_conj"]) <= tol
+
+
+def test_p0_evaluators_batched_instances_match_oracle():
+    models = [configs.make_model(3, i) for i in range(16)]
+    g = configs.CONFIGS[3].grid
+    idx = np.random.default_rng(5).integers(0, g.points_per_axis, size=(3000, 5))
+    vals = P.OracleBatch([P.PhiGridOracle(m, g) for m in models]).evaluate(idx, (65,) * 5)
+    for i, m in enumerate(models):
+        gm = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, g.n, g.eta, g.alpha)
+        assert rel(vals[i], gm.phi_oracle()(idx)) <= 1e-12
+
+
+# ------------------------------------------------------------------- P1
+def test_p1_contractions_match_reference(golden):
+    ct = load_npz("contractions.npz")
+    for q, meta in enumerate(golden["contractions"]):
+        phys, bonds = meta["phys"], uniform_bonds(len(meta["phys"]), meta["bond"])
+        a = tt_of(ct[f"t{q}_a"], phys, bonds)
+        b = tt_of(ct[f"t{q}_b"], phys, bonds)
+        inner = np.array([P.tt_inner(a, b), P.tt_inner(b, a), P.tt_inner(a, a)])
+        assert rel(inner, ct[f"t{q}_inner"]) <= 1e-12
+        assert rel(P.tt_evaluate_many(a, ct[f"t{q}_idx"]), ct[f"t{q}_eval"]) <= 1e-12
+        w = ct[f"t{q}_sepw"]
+        cuts = np.cumsum([0] + phys)
+        sep = P.SeparableOracle([w[cuts[k]:cuts[k + 1]] for k in range(len(phys))])
+        assert rel(P.tt_rand_sample_diff(a, sep, 5000, 17), ct[f"t{q}_diff"][0]) <= 1e-10
+        assert P.tt_rand_sample_diff(a, P.TTOracle(a), 700, 3) <= 1e-13
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_p1_inner_on_reference_cross_cores(golden, cid):
+    """K7 on the reference's own cross cores reproduces the reference's raw sum."""
+    pc = load_npz("prices_cores.npz")
+    spec = configs.CONFIGS[cid]
+    shape = (spec.grid.points_per_axis,) * spec.d
+    ranks = P.cross.rank_profile(shape, spec.bond_dim)
+    phi = tt_of(pc[f"cfg{cid}_i0_phi"], shape, ranks)
+    v = tt_of(pc[f"cfg{cid}_i0_v"], shape, ranks)
+    raw = P.tt_inner(v, phi)
+    want = complex(*golden["prices"][f"cfg{cid}_i0"]["raw"])
+    assert abs(raw - want) <= 1e-12 * abs(want)
+
+
+# ------------------------------------------------------------------- P2
+def test_p2_dense_sums_match_reference(golden):
+    dn = golden["dense"]
+    m1 = P.MarketModel(d=1, **BENCH)
+    for n in (30, 50):
+        assert rel(P.price_fourier_dense(m1, bench_grid(1, n)).price, dn[f"d1_n{n}"]) <= 1e-10
+    assert rel(P.price_fourier_dense(plus_model(2), bench_grid(2)).price, dn["d2_bench"]) <= 1e-10
+    assert rel(P.price_fourier_dense(plus_model(2), bench_grid(2), t=0.25).price, dn["d2_bench_t025"]) <= 1e-10
+    assert rel(P.price_fourier_dense(plus_model(3), bench_grid(3)).price, dn["d3_bench"]) <= 1e-10
+    assert rel(P.price_fourier_dense(configs.make_model(1), configs.CONFIGS[1].grid).price, dn["cfg1"]) <= 1e-10
+    g5 = P.GridSpec(n=16, eta=0.3, alpha=1.0, d=5)
+    got = [r.price for r in P.price_fourier_dense_batch([configs.make_model(3, i) for i in range(4)], g5)]
+    assert rel(got, dn["cfg3_n16"]) <= 1e-10
+
+
+def test_p2_dense_cfg2_full_grid(golden):
+    """The 65^5 = 1.16e9-term sum the reference needs ~13 minutes for."""
+    if "cfg2" not in golden["dense"]:
+        pytest.skip("cfg2 dense golden not generated")
+    got = P.price_fourier_dense(configs.make_model(2), configs.CONFIGS[2].grid,
+                                term_cap=2_000_000_000).price
+    assert rel(got, golden["dense"]["cfg2"]) <= 1e-10
+
+
+def test_p2_dense_errors():
+    with pytest.raises(P.CapacityError, match="132651"):
+        P.price_fourier_dense(plus_model(3), bench_grid(3), term_cap=1000)
+    with pytest.raises(P.StripConditionError):
+        P.price_fourier_dense(plus_model(2), P.GridSpec(n=10, eta=0.5, alpha=0.2, d=2))
+    with pytest.raises(ValueError):
+        P.price_fourier_dense(plus_model(2), bench_grid(3))
+
+
+# ------------------------------------------------------------------- P3
+def test_p3_maxvol_selections_identical_to_reference():
+    mv = load_npz("maxvol.npz")
+    q = 0
+    while f"m{q}" in mv:
+        np.testing.assert_array_equal(P.maxvol(mv[f"m{q}"], slack=0.01), mv[f"m{q}_sel"])
+        q += 1
+
+
+def test_p3_maxvol_property_suite():
+    # test_acceptance.py:118-143 / test_cross.py:37-57 (dominance, near-optimality)
+    from itertools import combinations
+    rng = np.random.default_rng(4)
+    shapes = [(8, 2), (12, 3), (24, 5), (48, 8), (64, 8)]
+    for q in range(100):
+        n, r = shapes[q % len(shapes)]
+        m = rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r))
+        rows = P.maxvol(m, slack=0.01)
+        np.testing.assert_array_equal(rows, O.maxvol(m, slack=0.01))
+        assert np.abs(m @ np.linalg.inv(m[rows])).max() <= 1.01 + 1e-9
+    rng = np.random.default_rng(0)
+    for n, r in [(6, 2), (8, 3), (10, 3)]:
+        for _ in range(25):
+            m = rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r))
+            rows = P.maxvol(m, slack=0.01)
+            got = abs(np.linalg.det(m[rows]))
+            best = max(abs(np.linalg.det(m[list(c)])) for c in combinations(range(n), r))
+            assert got >= best / 1.01 ** r - 1e-12
+
+
+def test_p3_maxvol_edge_cases():
+    np.testing.assert_array_equal(P.maxvol(np.array([[1.0], [10.0], [3.0]])), [1])
+    sq = np.random.default_rng(0).standard_normal((4, 4)) + 0j
+    np.testing.assert_array_equal(P.maxvol(sq), np.arange(4))
+    u = np.arange(1.0, 7.0)
+    with pytest.raises(P.SingularMatrixError):
+        P.maxvol(np.column_stack([u, 2 * u, -u]))
+    with pytest.raises(P.SingularMatrixError):
+        P.maxvol(np.zeros((5, 2)))
+    with pytest.raises(P.MaxvolIterationError):
+        P.maxvol(np.random.default_rng(1).standard_normal((30, 3)), slack=0.0, max_iters=0)
+    with pytest.raises(ValueError):
+        P.maxvol(np.ones((2, 3)))
+
+
+def _sep_weights(cr):
+    w = cr["sep_w"]
+    return [w[0:6], w[6:12], w[12:18]]
+
+
+def test_p3_cross_decisions_match_reference(golden):
+    cr = load_npz("cross.npz")
+    tt, rep = P.tt_cross(P.SeparableOracle(_sep_weights(cr)), (6, 6, 6),
+                         P.CrossConfig(bond_dim=1, eps_tol=1e-10, n_conv_samples=2000, seed=0))
+    g = golden["cross"]["sep"]
+    assert rep.converged and rep.sweeps_used == 1 and rep.final_diff <= 1e-10
+    assert rep.oracle_calls == g["oracle_calls"] and rep.conv_check_calls == g["conv_check_calls"]
+    assert sets_as_lists(rep.left_sets) == g["left_sets"]
+    assert sets_as_lists(rep.right_sets) == g["right_sets"]
+    target = tt_of(cr["selfrec_target"], (8, 8, 8, 8), uniform_bonds(4, 4))
+    tt, rep = P.tt_cross(P.TTOracle(target), (8, 8, 8, 8),
+                         P.CrossConfig(bond_dim=4, eps_tol=1e-8, n_conv_samples=5000, seed=3))
+    g = golden["cross"]["selfrec"]
+    assert rep.final_diff <= 1e-8
+    assert sets_as_lists(rep.left_sets) == g["left_sets"]
+    # the characteristic-function crosses whose blocks are well conditioned
+    for d, bond, seed, beta in ((2, 6, 7, 0.5), (3, 4, 17, 1.0)):
+        grid = bench_grid(d)
+        tt, rep = P.tt_cross(P.phi_grid_oracle(plus_model(d, beta), grid), (51,) * d,
+                             P.CrossConfig(bond_dim=bond, seed=seed, n_conv_samples=2000))
+        g = golden["cross"][f"phi_d{d}_D{bond}_s{seed}"]
+        assert rep.sweeps_used == g["sweeps_used"] and rep.converged == g["converged"]
+        assert rep.oracle_calls == g["oracle_calls"]
+        assert sets_as_lists(rep.left_sets) == g["left_sets"]
+        assert sets_as_lists(rep.right_sets) == g["right_sets"]
+        assert rel(rep.final_diff, g["final_diff"]) <= 1e-9
+
+
+def test_p3_cross_behaviours():
+    # reference test_cross.py:143-256 mirrored on the device path
+    grid = bench_grid(3)
+    oracle = P.phi_grid_oracle(plus_model(3, 0.5), grid)
+    _, rep = P.tt_cross(oracle, (51, 51, 51), P.CrossConfig(bond_dim=10, seed=101))
+    assert rep.converged and rep.sweeps_used == 1 and rep.final_diff <= 0.005
+    # interpolation property at the cross indices
+    g2 = bench_grid(2)
+    o2 = P.phi_grid_oracle(plus_model(2, 0.5), g2)
+    tt, rep = P.tt_cross(o2, (51, 51), P.CrossConfig(bond_dim=6, seed=7, n_conv_samples=2000))
+    idx = np.array([a + b for k in range(1, tt.d) for a in rep.left_sets[k] for b in rep.right_sets[k]])
+    got = P.tt_evaluate_many(tt, idx)
+    want = o2(idx)
+    assert np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300))
+    # budget error, d=1, non-convergence
+    w = [np.random.default_rng(1).standard_normal(8) for _ in range(3)]
+    with pytest.raises(P.OracleBudgetError):
+        P.tt_cross(P.SeparableOracle(w), (8, 8, 8),
+                   P.CrossConfig(bond_dim=2, n_conv_samples=100, seed=0, oracle_call_budget=50))
+    vals = np.arange(1.0, 8.0) + 0.5j
+    tt, rep = P.tt_cross(P.TableOracle(vals), (7,), P.CrossConfig(bond_dim=3, n_conv_samples=100, seed=0))
+    assert rep.converged and rep.final_diff == 0.0
+    np.testing.assert_array_equal(tt.cores[0][0, :, 0], vals)
+    o3 = P.phi_grid_oracle(plus_model(3, 1.0), grid)
+    _, rep = P.tt_cross(o3, (51, 51, 51), P.CrossConfig(bond_dim=2, max_sweeps=1, n_conv_samples=2000, seed=0))
+    assert not rep.converged and rep.final_diff > 0.005
+    diffs = []
+    for sweeps in (1, 2, 3, 4):
+        tt, rep = P.tt_cross(o3, (51, 51, 51), P.CrossConfig(bond_dim=4, eps_tol=1e-14, max_sweeps=sweeps,
+                                                             n_conv_samples=3000, seed=17))
+        assert rep.sweeps_used == sweeps and tt.phys_dims == (51, 51, 51)
+        diffs.append(rep.final_diff)
+    assert all(np.isfinite(diffs)) and min(diffs[1:]) <= 5 * diffs[0]
+
+
+def test_p3_cross_call_scaling_and_determinism():
+    target_cores = [np.random.default_rng(21).standard_normal((b0, 9, b1)) + 0j
+                    for b0, b1 in ((1, 3), (3, 3), (3, 3), (3, 1))]
+    target = P.TensorTrain(target_cores)
+    _, rep = P.tt_cross(P.TTOracle(target), (9,) * 4, P.CrossConfig(bond_dim=3, n_conv_samples=1000, seed=2))
+    assert rep.oracle_calls <= 10 * 4 * 9 * 9
+    assert rep.compression_ratio == rep.oracle_calls / 9 ** 4
+    grid = bench_grid(2)
+    o = P.phi_grid_oracle(plus_model(2, 0.5), grid)
+    cfg = P.CrossConfig(bond_dim=5, seed=31, n_conv_samples=2000)
+    t1, r1 = P.tt_cross(o, (51, 51), cfg)
+    t2, r2 = P.tt_cross(o, (51, 51), cfg)
+    assert r1.to_dict() == r2.to_dict() and r1.left_sets == r2.left_sets and r1.right_sets == r2.right_sets
+    for a, b in zip(t1.cores, t2.cores):
+        np.testing.assert_array_equal(a, b)
+
+
+# ------------------------------------------------------------------- P4
+# The reference is not reproducible at 1e-8 end to end: 1
+# vs 8 BLAS threads moves cfg2 by 1.3e-6 and a 1e-15 oracle perturbation
+# moves cfg1/cfg2/cfg4 by 8.8e-6 / 4.3e-4 / 5.9e-6.  The bands below are
+# those measured floors (x2); dense-sum checks use the reference's own
+# truncation error as the yardstick.
+P4_BAND = {1: 2e-5, 2: 1e-3, 3: 1e-3, 4: 2e-5}
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+def test_p4_prices_within_reference_band(golden, cid):
+    spec = configs.CONFIGS[cid]
+    n_inst = 1 if cid in (1, 2, 4) else 4
+    models = [configs.make_model(cid, i) for i in range(n_inst)]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    res = P.price_fourier_tt_batch(models, spec.grid, cfg, cfg)
+    for i, r in enumerate(res):
+        ref = golden["prices"][f"cfg{cid}_i{i}"]
+        assert rel(r.price, ref["price"]) <= P4_BAND[cid]
+        assert r.diagnostics["cross_phi"].oracle_calls == ref["cross_phi"]["oracle_calls"]
+        assert r.diagnostics["cross_v"].sweeps_used == ref["cross_v"]["sweeps_used"]
+
+
+def test_p4_cfg1_against_dense(golden):
+    spec = configs.CONFIGS[1]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    res = P.price_fourier_tt(configs.make_model(1), spec.grid, cfg, cfg)
+    dense = golden["dense"]["cfg1"]
+    ref_eps = abs(golden["prices"]["cfg1_i0"]["price"] - dense) / dense
+    assert res.diagnostics["dense_price"] == pytest.approx(dense, rel=1e-10)
+    assert res.diagnostics["eps_trunc"] <= max(1e-4, 3 * ref_eps)
+
+
+def test_p4_cfg2_against_dense(golden):
+    if "cfg2" not in golden["dense"]:
+        pytest.skip("cfg2 dense golden not generated")
+    spec = configs.CONFIGS[2]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    res = P.price_fourier_tt(configs.make_model(2), spec.grid, cfg, cfg, dense_reference="never")
+    dense = golden["dense"]["cfg2"]
+    ref_eps = abs(golden["prices"]["cfg2_i0"]["price"] - dense) / dense
+    assert abs(res.price - dense) / dense <= max(1e-4, 3 * ref_eps)
+
+
+def test_p4_reference_pricer_tests():
+    # test_pricers.py:125-172 and test_acceptance.py:64-72 on the device path
+    m = P.MarketModel(d=1, **BENCH)
+    grid = bench_grid(1)
+    dense = P.price_fourier_dense(m, grid).price
+    cfg = P.CrossConfig(bond_dim=1, seed=0, n_conv_samples=1000)
+    res = P.price_fourier_tt(m, grid, cfg, cfg)
+    assert abs(res.price - dense) <= 1e-10 * abs(dense)
+    assert res.diagnostics["cross_phi"].converged and res.diagnostics["cross_v"].converged
+    for d in (2, 3, 4):
+        eta, bond_v, bond_phi = P.table1_hyperparams(d)
+        r = P.price_fourier_tt(plus_model(d), bench_grid(d), P.CrossConfig(bond_dim=bond_phi, seed=1234 + d),
+                               P.CrossConfig(bond_dim=bond_v, seed=1234 + d))
+        assert r.diagnostics["eps_trunc"] <= (1e-5 if d in (2, 4) else 1e-4)
+    r = P.price_fourier_tt(plus_model(10), bench_grid(10), P.CrossConfig(bond_dim=20, seed=1244),
+                           P.CrossConfig(bond_dim=40, seed=1244))
+    assert "eps_trunc" not in r.diagnostics
+    assert r.diagnostics["oracle_calls_total"] / bench_grid(10).n_terms <= 1e-9
+    m3 = plus_model(3, 1.0)
+    cfg = P.CrossConfig(bond_dim=2, max_sweeps=1, seed=0, n_conv_samples=2000)
+    r = P.price_fourier_tt(m3, bench_grid(3), cfg, cfg, dense_reference="never")
+    assert np.isfinite(r.price) and not r.diagnostics["cross_phi"].converged
+    m2 = plus_model(2)
+    cfg = P.CrossConfig(bond_dim=6, seed=3, n_conv_samples=1000)
+    base = P.price_fourier_tt(m2, bench_grid(2), cfg, cfg, dense_reference="never").price
+    shifted = P.price_fourier_tt(m2, bench_grid(2), cfg, cfg, t=0.25, dense_reference="never").price
+    assert shifted == pytest.approx(base * np.exp(m2.r * 0.25), rel=1e-12)
+
+
+# --------------------------------------------- full-size, size-independent
+def test_full_size_cfg4_batch_properties():
+    """At the benchmark size: batch == single bitwise, the interpolation
+    property at the final pivots, and K6/K7 against the CPU oracle on the
+    device-built cores."""
+    spec = configs.CONFIGS[4]
+    models = [configs.make_model(4, i) for i in range(3)]
+    shape = (spec.grid.points_per_axis,) * spec.d
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    batch = P.tt_cross_batch([P.PhiGridOracle(m, spec.grid) for m in models], shape, cfg)
+    assert all(s == 0 for s in batch.status)
+    trains = batch.trains.to_trains()
+    single_tt, single_rep = P.tt_cross(P.PhiGridOracle(models[1], spec.grid), shape, cfg)
+    for a, b in zip(trains[1].cores, single_tt.cores):
+        np.testing.assert_array_equal(a, b)
+    assert single_rep.to_dict() == batch.reports[1].to_dict()
+    for i, m in enumerate(models):
+        rep, tt = batch.reports[i], trains[i]
+        oracle = P.PhiGridOracle(m, spec.grid)
+        k = spec.d // 2
+        idx = np.array([a + b for a in rep.left_sets[k] for b in rep.right_sets[k]])
+        got = P.tt_evaluate_many(tt, idx)
+        want = oracle(idx)
+        assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))
+        gm = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, spec.grid.n, spec.grid.eta, spec.grid.alpha)
+        cpu_diff = O.sample_diff(list(tt.cores), gm.phi_oracle(), cfg.n_conv_samples, cfg.seed)
+        assert abs(cpu_diff - rep.final_diff) <= 1e-9 * max(cpu_diff, 1e-300) + 1e-15
+        assert abs(P.tt_inner(tt, tt) - O.tt_inner(tt.cores, tt.cores)) <= 1e-12 * abs(O.tt_inner(tt.cores, tt.cores))
+
+
+def test_batch_prices_equal_single_prices():
+    spec = configs.CONFIGS[3]
+    models = [configs.make_model(3, i) for i in range(6)]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    batch = P.price_fourier_tt_batch(models, spec.grid, cfg, cfg)
+    for i in (0, 4):
+        single = P.price_fourier_tt(models[i], spec.grid, cfg, cfg, dense_reference="never")
+        assert single.price == batch[i].price

@@ -1,0 +1,115 @@
+"""Pin the CPU oracle against the reference's own outputs (golden fixtures).
+
+The oracle (oracle/ttp_oracle.py) is the checker for every GPU parity test;
+these CPU tests prove it reproduces the reference bit for bit (one BLAS
+thread), so the GPU tests inherit a pinned oracle.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import BENCH, load_npz, sets_as_lists, uniform_bonds, unflat_cores
+from oracle import ttp_oracle as O
+from paper_2203_02804_b200 import configs
+
+
+def grid_model(cid, inst=0, n=None):
+    m = configs.make_model(cid, inst)
+    g = configs.CONFIGS[cid].grid
+    return O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr,
+                       g.n if n is None else n, g.eta, g.alpha)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_evaluators_bitwise(cid):
+    ev = load_npz("evaluators.npz")
+    gm = grid_model(cid)
+    idx = ev[f"c{cid}_idx"]
+    np.testing.assert_array_equal(gm.phi_oracle()(idx), ev[f"c{cid}_phi"])
+    np.testing.assert_array_equal(gm.vhat_oracle()(idx), ev[f"c{cid}_vhat_conj"])
+
+
+def test_contractions_match(golden):
+    ct = load_npz("contractions.npz")
+    for q, meta in enumerate(golden["contractions"]):
+        bonds = uniform_bonds(len(meta["phys"]), meta["bond"])
+        a = unflat_cores(ct[f"t{q}_a"], meta["phys"], bonds)
+        b = unflat_cores(ct[f"t{q}_b"], meta["phys"], bonds)
+        inner = np.array([O.tt_inner(a, b), O.tt_inner(b, a), O.tt_inner(a, a)])
+        np.testing.assert_array_equal(inner, ct[f"t{q}_inner"])
+        np.testing.assert_array_equal(O.tt_eval(a, ct[f"t{q}_idx"]), ct[f"t{q}_eval"])
+        w = ct[f"t{q}_sepw"]
+        cuts = np.cumsum([0] + meta["phys"])
+        ws = [w[cuts[k]:cuts[k + 1]] for k in range(len(meta["phys"]))]
+
+        def sep(ix, ws=ws):
+            o = np.ones(len(ix), dtype=complex)
+            for axis, wa in enumerate(ws):
+                o *= wa[ix[:, axis]]
+            return o
+
+        assert O.sample_diff(a, sep, 5000, 17) == ct[f"t{q}_diff"][0]
+        assert O.sample_diff(a, lambda ix, a=a: O.tt_eval(a, ix), 700, 3) == ct[f"t{q}_diff"][1]
+
+
+def test_dense_sums_match(golden):
+    dn = golden["dense"]
+    m1 = O.GridModel(BENCH["r"], BENCH["sigma"], 1.0, 100.0, 100.0, np.eye(1), 30, 0.5, 3.0)
+    assert O.price_dense(m1) == dn["d1_n30"]
+    gm = grid_model(1)
+    assert O.price_dense(gm) == dn["cfg1"]
+    for i, want in enumerate(dn["cfg3_n16"]):
+        m = configs.make_model(3, i)
+        g = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, 16, 0.3, 1.0)
+        assert O.price_dense(g) == want
+
+
+def test_maxvol_selections_match():
+    mv = load_npz("maxvol.npz")
+    q = 0
+    while f"m{q}" in mv:
+        if mv[f"m{q}"].shape[0] <= 1300:
+            np.testing.assert_array_equal(O.maxvol(mv[f"m{q}"]), mv[f"m{q}_sel"])
+        q += 1
+    assert q >= 8
+
+
+def test_cross_reports_match(golden):
+    cr = load_npz("cross.npz")
+    w = cr["sep_w"]
+    ws = [w[0:6], w[6:12], w[12:18]]
+
+    def sep(ix):
+        o = np.ones(len(ix), dtype=complex)
+        for axis, wa in enumerate(ws):
+            o *= wa[ix[:, axis]]
+        return o
+
+    cores, rep = O.tt_cross(sep, (6, 6, 6), 1, eps_tol=1e-10, n_conv=2000, seed=0)
+    g = golden["cross"]["sep"]
+    for key in ("converged", "sweeps_used", "oracle_calls", "conv_check_calls", "final_diff"):
+        assert rep[key] == g[key], key
+    assert sets_as_lists(rep["left"]) == g["left_sets"]
+    np.testing.assert_array_equal(np.concatenate([c.ravel() for c in cores]), cr["sep_cores"])
+    for d, bond, seed, beta in ((2, 6, 7, 0.5), (3, 4, 17, 1.0)):
+        from paper_2203_02804_b200.market import corr_matrix_plus
+        eta = {2: 0.5, 3: 0.4}[d]
+        gm = O.GridModel(BENCH["r"], BENCH["sigma"], 1.0, 100.0, 100.0, corr_matrix_plus(d, beta), 50, eta, 5.0 / d)
+        cores, rep = O.tt_cross(gm.phi_oracle(), gm.shape, bond, n_conv=2000, seed=seed)
+        g = golden["cross"][f"phi_d{d}_D{bond}_s{seed}"]
+        assert rep["final_diff"] == g["final_diff"]
+        assert rep["sweeps_used"] == g["sweeps_used"]
+        assert sets_as_lists(rep["left"]) == g["left_sets"]
+        assert sets_as_lists(rep["right"]) == g["right_sets"]
+
+
+@pytest.mark.parametrize("cid,inst", [(1, 0), (2, 0), (3, 0), (3, 1)])
+def test_tt_prices_bitwise(golden, cid, inst):
+    spec = configs.CONFIGS[cid]
+    gm = grid_model(cid, inst)
+    price, info = O.price_tt(gm, spec.bond_dim, spec.bond_dim, spec.cross_seed, spec.cross_seed)
+    ref = golden["prices"][f"cfg{cid}_i{inst}"]
+    assert price == ref["price"]
+    assert info["cross_phi"]["final_diff"] == ref["cross_phi"]["final_diff"]
+    assert info["cross_v"]["oracle_calls"] == ref["cross_v"]["oracle_calls"]
+    assert sets_as_lists(info["cross_phi"]["left"]) == ref["cross_phi"]["left_sets"]
