@@ -142,9 +142,26 @@ typedef struct ttp_cross_out {
   double* h_final_diff;      /* host, n_inst                                  */
 } ttp_cross_out;
 
+/* Per-kernel-class launch statistics (diagnostics; see ttp_profile_read). */
+typedef struct ttp_kernel_stat {
+  char name[32];
+  int64_t launches;        /* kernels launched since the last reset          */
+  int64_t timed_launches;  /* of which bracketed by CUDA events              */
+  double total_ms;         /* summed device time of the timed launches       */
+} ttp_kernel_stat;
+
 int ttp_abi_version(void);
 const char* ttp_last_error(void);
 int ttp_device_count(void);
+
+/* Diagnostics: total kernel launches issued by this library (monotone), and
+ * optional CUDA-event timing of every launch on its own stream.  Reading
+ * synchronises on the recorded events; enabling adds two event records per
+ * launch and no host synchronisation.                                       */
+int64_t ttp_launch_count(void);
+void ttp_profile_enable(int on);
+void ttp_profile_reset(void);
+int ttp_profile_read(ttp_kernel_stat* out, int32_t max_entries);
 
 /* K1/K2 fiber evaluators at explicit multi-indices (shared by all
  * instances): d_out[i*m + j] = oracle_i(d_idx[j, :]).

@@ -127,11 +127,24 @@ class CrossOut(ctypes.Structure):
     ]
 
 
+class KernelStat(ctypes.Structure):
+    _fields_ = [
+        ("name", ctypes.c_char * 32),
+        ("launches", _i64),
+        ("timed_launches", _i64),
+        ("total_ms", _f64),
+    ]
+
+
 # (name, restype, argtypes) for every symbol declared in include/ttpricer_b200.h
 SIGNATURES = [
     ("ttp_abi_version", _i32, []),
     ("ttp_last_error", ctypes.c_char_p, []),
     ("ttp_device_count", _i32, []),
+    ("ttp_launch_count", _i64, []),
+    ("ttp_profile_enable", None, [ctypes.c_int]),
+    ("ttp_profile_reset", None, []),
+    ("ttp_profile_read", _i32, [ctypes.POINTER(KernelStat), _i32]),
     ("ttp_oracle_eval", _i32, [ctypes.POINTER(Oracle), _p, _i32, _p, _i64, _p, _p]),
     ("ttp_tt_inner", _i32, [ctypes.POINTER(TTBatch), ctypes.POINTER(TTBatch), _p, _p]),
     ("ttp_tt_eval_workspace", _sz, [ctypes.POINTER(TTBatch), _i64]),
@@ -211,6 +224,27 @@ def require_device():
             "no CUDA device visible: the B200 pricer has no CPU fallback"
         )
     return torch
+
+
+def launch_count():
+    """Kernels launched by the library so far (diagnostic counter)."""
+    return int(load_library().ttp_launch_count())
+
+
+def profile_enable(on=True):
+    load_library().ttp_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    load_library().ttp_profile_reset()
+
+
+def profile_read():
+    """{kernel class: (launches, timed_launches, total_ms)} since the last reset."""
+    arr = (KernelStat * 32)()
+    n = load_library().ttp_profile_read(arr, 32)
+    return {arr[i].name.decode(): (int(arr[i].launches), int(arr[i].timed_launches),
+                                   float(arr[i].total_ms)) for i in range(n)}
 
 
 def stream_handle():

@@ -173,6 +173,7 @@ class CrossBatchResult:
     reports: list
     status: np.ndarray
     error_bond: np.ndarray
+    counters: dict = None
 
     def error_for(self, i):
         return _status_error(int(self.status[i]), int(self.error_bond[i]))
@@ -190,7 +191,7 @@ def _status_error(status, bond):
     return RuntimeError(f"cross failed with status {status}")
 
 
-def tt_cross_batch(oracles, shape, cfg):
+def tt_cross_batch(oracles, shape, cfg, with_reports=True):
     """Batched TT-cross of independent oracles sharing ``shape`` and ``cfg``.
 
     Returns a :class:`CrossBatchResult` whose trains stay on the GPU; per
@@ -260,6 +261,8 @@ def tt_cross_batch(oracles, shape, cfg):
     _lib.raise_for(st, "tt_cross")
     del ws
     trains = DeviceTTBatch(shape, ranks, cores, n)
+    if not with_reports:
+        return CrossBatchResult(trains, None, h["status"].copy(), h["bond"].copy(), h)
     left_h = left.cpu().numpy().reshape(n, lay.set_stride)
     right_h = right.cpu().numpy().reshape(n, lay.set_stride)
     total = math.prod(shape)
@@ -282,7 +285,7 @@ def tt_cross_batch(oracles, shape, cfg):
             left_sets=lsets,
             right_sets=rsets,
         ))
-    return CrossBatchResult(trains, reports, h["status"].copy(), h["bond"].copy())
+    return CrossBatchResult(trains, reports, h["status"].copy(), h["bond"].copy(), h)
 
 
 def tt_cross(oracle, shape, cfg):

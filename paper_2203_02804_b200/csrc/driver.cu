@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "ttp_internal.h"
+#include "launch.h"
 #include "k_bond.h"
 
 // conv-check kernels from k_tt.cu
@@ -191,8 +192,11 @@ int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const 
   {
     const long long tot = M * r1;
     dim3 grid((unsigned)((tot + 255) / 256), (unsigned)n);
-    conv_site0_kernel<<<grid, 256, 0, s>>>(cores, L.core_stride, L.core_offsets[0], r1, P.d_conv_idx,
-                                           d, M, w.V0, w.v_stride, d_active);
+    {
+      LaunchScope _ls(KC_CONV_SITE0, s);
+      conv_site0_kernel<<<grid, 256, 0, s>>>(cores, L.core_stride, L.core_offsets[0], r1, P.d_conv_idx,
+                                             d, M, w.V0, w.v_stride, d_active);
+    }
   }
   cplx* vin = w.V0;
   cplx* vout = w.V1;
@@ -203,14 +207,20 @@ int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const 
       const size_t smem = sizeof(cplx) * ra * rb;
       TTP_CUDA_CHECK(cudaFuncSetAttribute(conv_site_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       dim3 grid((unsigned)nk, (unsigned)n);
-      conv_site_kernel<<<grid, 256, smem, s>>>(cores, L.core_stride, L.core_offsets[k], ra, nk, rb,
-                                               P.d_conv_perm + (long long)k * M, P.d_conv_off + goff,
-                                               vin, vout, w.v_stride, d_active);
+      {
+        LaunchScope _ls(KC_CONV_SITE, s);
+        conv_site_kernel<<<grid, 256, smem, s>>>(cores, L.core_stride, L.core_offsets[k], ra, nk, rb,
+                                                 P.d_conv_perm + (long long)k * M, P.d_conv_off + goff,
+                                                 vin, vout, w.v_stride, d_active);
+      }
       std::swap(vin, vout);
     }
     goff += P.h_shape[k] + 1;
   }
-  sample_diff_kernel<<<n, 1024, 0, s>>>(w.exact, vin, M, M, w.v_stride, w.diff, d_active);
+  {
+    LaunchScope _ls(KC_SAMPLE_DIFF, s);
+    sample_diff_kernel<<<n, 1024, 0, s>>>(w.exact, vin, M, M, w.v_stride, w.diff, d_active);
+  }
   TTP_CUDA_CHECK(cudaGetLastError());
   return TTP_OK;
 }
@@ -252,7 +262,10 @@ extern "C" int ttp_cross_run(const ttp_cross_problem* prob, ttp_cross_out* out, 
   // initial right sets (same draw for every instance: cross.py:402-403)
   {
     dim3 grid((unsigned)((L.set_stride + 255) / 256), (unsigned)n);
-    replicate_kernel<<<grid, 256, 0, s>>>(P.d_right_init, L.set_stride, out->d_right, L.set_stride);
+    {
+      LaunchScope _ls(KC_MISC, s);
+      replicate_kernel<<<grid, 256, 0, s>>>(P.d_right_init, L.set_stride, out->d_right, L.set_stride);
+    }
     TTP_CUDA_CHECK(cudaMemsetAsync(out->d_left, 0, sizeof(int) * L.set_stride * n, s));
   }
   // exact oracle values at the convergence samples: identical every sweep
@@ -490,7 +503,10 @@ extern "C" int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const doubl
   bj.write_mode = 0;
   {
     dim3 grid((unsigned)((mr + 255) / 256), (unsigned)n_mat);
-    to_colmajor_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const cplx*>(d_mats), rows, cols, bj.A, mr);
+    {
+      LaunchScope _ls(KC_MISC, s);
+      to_colmajor_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const cplx*>(d_mats), rows, cols, bj.A, mr);
+    }
   }
   TTP_CUDA_CHECK(cudaMemsetAsync(bj.status, 0, sizeof(int) * n_mat, s));
   TTP_CUDA_CHECK(launch_bond(bj, n_mat, s));

@@ -20,6 +20,7 @@
 // "first maximum" tie-breaks follow the reference's scan order exactly.
 // All reductions are fixed-order (warp xor trees + ordered warp merge).
 #include "ttp_internal.h"
+#include "launch.h"
 #include "k_bond.h"
 
 #include <float.h>
@@ -845,6 +846,9 @@ cudaError_t launch_bond(const BondJob& job, int n_inst, cudaStream_t s) {
   const size_t smem = bond_smem_bytes(job.r);
   cudaError_t e = cudaFuncSetAttribute(bond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  bond_kernel<<<n_inst, NT, smem, s>>>(job);
+  {
+    LaunchScope _ls(KC_BOND, s);
+    bond_kernel<<<n_inst, NT, smem, s>>>(job);
+  }
   return cudaGetLastError();
 }

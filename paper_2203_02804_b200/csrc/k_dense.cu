@@ -8,6 +8,7 @@
 // bound, not HBM bound) and the per-slab sums are combined in slab order by
 // a second kernel, so the result is independent of scheduling.
 #include "ttp_internal.h"
+#include "launch.h"
 
 namespace {
 
@@ -96,9 +97,15 @@ extern "C" int ttp_dense_sum(const ttp_oracle* phi, const ttp_oracle* vhat, cons
   cplx* part = reinterpret_cast<cplx*>(d_ws);
   cplx* out = part + (size_t)n_inst * DENSE_SLABS;
   dim3 grid(DENSE_SLABS, (unsigned)n_inst);
-  dense_partial_kernel<<<grid, DENSE_THREADS, 0, s>>>(a, b, n_terms, part);
+  {
+    LaunchScope _ls(KC_DENSE, s);
+    dense_partial_kernel<<<grid, DENSE_THREADS, 0, s>>>(a, b, n_terms, part);
+  }
   TTP_CUDA_CHECK(cudaGetLastError());
-  dense_final_kernel<<<n_inst, 256, 0, s>>>(part, DENSE_SLABS, out);
+  {
+    LaunchScope _ls(KC_DENSE_FINAL, s);
+    dense_final_kernel<<<n_inst, 256, 0, s>>>(part, DENSE_SLABS, out);
+  }
   TTP_CUDA_CHECK(cudaGetLastError());
   TTP_CUDA_CHECK(cudaMemcpyAsync(h_out, out, sizeof(cplx) * n_inst, cudaMemcpyDeviceToHost, s));
   TTP_CUDA_CHECK(cudaStreamSynchronize(s));

@@ -8,6 +8,7 @@
 // factorizes: one thread per entry, consecutive threads on consecutive rows
 // so the complex128 stores coalesce.
 #include "ttp_internal.h"
+#include "launch.h"
 
 namespace {
 
@@ -63,7 +64,10 @@ void launch_fiber(const OracleDev& o, const FiberJob& job, const int* active, in
   if (total == 0 || n_inst == 0) return;
   const int threads = 256;
   dim3 grid((unsigned)((total + threads - 1) / threads), (unsigned)n_inst);
-  fiber_kernel<<<grid, threads, 0, s>>>(o, job, active);
+  {
+    LaunchScope _ls(KC_FIBER, s);
+    fiber_kernel<<<grid, threads, 0, s>>>(o, job, active);
+  }
 }
 
 void launch_oracle_points(const OracleDev& o, int n_inst, const int* idx, long long m,
@@ -71,5 +75,8 @@ void launch_oracle_points(const OracleDev& o, int n_inst, const int* idx, long l
   if (m == 0 || n_inst == 0) return;
   const int threads = 256;
   dim3 grid((unsigned)((m + threads - 1) / threads), (unsigned)n_inst);
-  points_kernel<<<grid, threads, 0, s>>>(o, idx, m, out);
+  {
+    LaunchScope _ls(KC_ORACLE_POINTS, s);
+    points_kernel<<<grid, threads, 0, s>>>(o, idx, m, out);
+  }
 }

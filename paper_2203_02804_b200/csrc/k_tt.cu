@@ -15,6 +15,7 @@
 //        s through it.  Each slice is read from HBM once per sweep instead
 //        of once per sample.
 #include "ttp_internal.h"
+#include "launch.h"
 
 namespace {
 
@@ -247,8 +248,11 @@ extern "C" int ttp_tt_inner(const ttp_tt_batch* bra, const ttp_tt_batch* ket, do
   }
   const size_t smem = sizeof(cplx) * (size_t)(2 * maxb * maxk);
   TTP_CUDA_CHECK(cudaFuncSetAttribute(tt_inner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  tt_inner_kernel<<<bra->n_inst, INNER_THREADS, smem, (cudaStream_t)stream>>>(
-      b, k, reinterpret_cast<cplx*>(d_out));
+  {
+    LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);
+    tt_inner_kernel<<<bra->n_inst, INNER_THREADS, smem, (cudaStream_t)stream>>>(
+        b, k, reinterpret_cast<cplx*>(d_out));
+  }
   TTP_CUDA_CHECK(cudaGetLastError());
   return TTP_OK;
 }
@@ -261,8 +265,11 @@ extern "C" int ttp_tt_eval(const ttp_tt_batch* tt, const int32_t* d_idx, int64_t
   if (m == 0 || tt->n_inst == 0) return TTP_OK;
   TTDev t = tt_dev(*tt);
   dim3 grid((unsigned)((m + EVAL_WARPS - 1) / EVAL_WARPS), (unsigned)tt->n_inst);
-  eval_warp_kernel<<<grid, EVAL_WARPS * 32, 0, (cudaStream_t)stream>>>(
-      t, d_idx, m, reinterpret_cast<cplx*>(d_out));
+  {
+    LaunchScope _ls(KC_TT_EVAL, (cudaStream_t)stream);
+    eval_warp_kernel<<<grid, EVAL_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        t, d_idx, m, reinterpret_cast<cplx*>(d_out));
+  }
   TTP_CUDA_CHECK(cudaGetLastError());
   return TTP_OK;
 }
@@ -275,9 +282,12 @@ extern "C" int ttp_sample_diff(int32_t n_inst, int64_t m, const double* d_exact,
     return ttp_fail(TTP_ERR_WORKSPACE, "sample_diff: workspace too small");
   if (n_inst == 0) return TTP_OK;
   double* sums = reinterpret_cast<double*>(d_ws);
-  sample_diff_kernel<<<n_inst, 1024, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const cplx*>(d_exact), reinterpret_cast<const cplx*>(d_approx), m, m, m,
-      sums, nullptr);
+  {
+    LaunchScope _ls(KC_SAMPLE_DIFF, (cudaStream_t)stream);
+    sample_diff_kernel<<<n_inst, 1024, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const cplx*>(d_exact), reinterpret_cast<const cplx*>(d_approx), m, m, m,
+        sums, nullptr);
+  }
   TTP_CUDA_CHECK(cudaGetLastError());
   std::string err;
   double* host = new double[2 * (size_t)n_inst];
