@@ -223,6 +223,7 @@ def main():
     import paper_2203_02804_b200 as P
     from paper_2203_02804_b200 import _lib, configs
     from paper_2203_02804_b200.distributed import gather_records, results_to_records, shard_range
+    from paper_2203_02804_b200.pricers import run_cross_pair
 
     sp = spec()
     grid = sp.grid
@@ -239,8 +240,7 @@ def main():
     v_batch = P.OracleBatch([P.PayoffGridOracle(m, grid, conj=True) for m in models])
 
     def device_step():
-        rp = P.tt_cross_batch(phi_batch, shape, cfg, with_reports=False)
-        rv = P.tt_cross_batch(v_batch, shape, cfg, with_reports=False)
+        rp, rv = run_cross_pair(phi_batch, v_batch, shape, cfg, cfg, with_reports=False)
         raw = P.tt_inner_batch(rv.trains, rp.trains)
         return prefs * raw.real, rp, rv
 

@@ -145,6 +145,7 @@ SIGNATURES = [
     ("ttp_profile_enable", None, [ctypes.c_int]),
     ("ttp_profile_reset", None, []),
     ("ttp_profile_read", _i32, [ctypes.POINTER(KernelStat), _i32]),
+    ("ttp_debug_phase_clocks", _i32, [ctypes.c_int, ctypes.POINTER(_i64), _i32]),
     ("ttp_oracle_eval", _i32, [ctypes.POINTER(Oracle), _p, _i32, _p, _i64, _p, _p]),
     ("ttp_tt_inner", _i32, [ctypes.POINTER(TTBatch), ctypes.POINTER(TTBatch), _p, _p]),
     ("ttp_tt_eval_workspace", _sz, [ctypes.POINTER(TTBatch), _i64]),

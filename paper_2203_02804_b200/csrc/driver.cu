@@ -183,6 +183,61 @@ SetView set_view(const int* base, const ttp_cross_layout& L, int k, int d) {
   return v;
 }
 
+// TTP_BOND_PATH=v0 forces the one-CTA-per-instance global-memory kernel
+// (k_bond_v0.cu); default is the cluster kernel whenever the block fits in
+// the cluster's distributed shared memory.
+// TTP_BOND_PATH: "v0" / "cluster" force a path; default "auto" picks the
+// cluster kernel when the batch fits in about two waves of clusters (latency
+// bound regime) and the one-CTA-per-instance kernel for large batches, where
+// occupying every SM wins.
+int bond_path_mode() {
+  static const int v = [] {
+    const char* e = getenv("TTP_BOND_PATH");
+    if (e && std::strcmp(e, "v0") == 0) return 1;
+    if (e && std::strcmp(e, "cluster") == 0) return 2;
+    return 0;
+  }();
+  return v;
+}
+bool force_v0() { return bond_path_mode() == 1; }
+
+size_t smem_optin_limit() {
+  static size_t lim = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 0;
+    return (size_t)v;
+  }();
+  return lim;
+}
+
+// One bond for every active instance: fibers + column basis + maxvol +
+// factor.  Cluster kernel (fibers evaluated in shared memory) when the block
+// fits, otherwise the fiber kernel followed by the global-memory bond kernel.
+int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const CrossWs& w, int n,
+             cudaStream_t s) {
+  const int C = force_v0() ? 0 : pick_cluster_size(bj.m, bj.r, smem_optin_limit());
+  if (C > 0) {
+    ClusterJob cj{};
+    cj.b = bj;
+    cj.cl = C;
+    cj.src_mode = 0;
+    cj.oracle = o;
+    cj.fiber = f;
+    cj.Qg = w.A;
+    cj.q_stride = w.mat_stride;
+    const int act = max_active_clusters(cj);
+    const bool use = act > 0 && (bond_path_mode() == 2 || n <= 2 * act);
+    if (use) {
+      TTP_CUDA_CHECK(launch_cluster_bond(cj, n, s));
+      return TTP_OK;
+    }
+  }
+  launch_fiber(o, f, w.active, n, s);
+  TTP_CUDA_CHECK(launch_bond(bj, n, s));
+  return TTP_OK;
+}
+
 int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const CrossWs& w,
                    const ttp_cross_out& out, const int* d_active, cudaStream_t s) {
   const int d = P.d, n = P.n_inst;
@@ -355,7 +410,6 @@ extern "C" int ttp_cross_run(const ttp_cross_problem* prob, ttp_cross_out* out, 
         f.out = w.A;
         f.out_stride = w.mat_stride;
         f.ld = (long long)f.rl * f.na;
-        launch_fiber(o, f, w.active, n, s);
         bj.m = f.rl * f.na;
         bj.r = L.ranks[k];
         bj.write_mode = 1;
@@ -368,7 +422,8 @@ extern "C" int ttp_cross_run(const ttp_cross_problem* prob, ttp_cross_out* out, 
         bj.bond = k;
         bj.na = P.h_shape[k - 1];
         bj.rr = 1;
-        TTP_CUDA_CHECK(launch_bond(bj, n, s));
+        st = run_bond(o, f, bj, w, n, s);
+        if (st != TTP_OK) return st;
       }
       FiberJob f{};
       f.mode = 0;
@@ -395,7 +450,6 @@ extern "C" int ttp_cross_run(const ttp_cross_problem* prob, ttp_cross_out* out, 
         f.out = w.A;
         f.out_stride = w.mat_stride;
         f.ld = (long long)f.na * f.rr;
-        launch_fiber(o, f, w.active, n, s);
         bj.m = f.na * f.rr;
         bj.r = L.ranks[k];
         bj.write_mode = 2;
@@ -408,7 +462,8 @@ extern "C" int ttp_cross_run(const ttp_cross_problem* prob, ttp_cross_out* out, 
         bj.bond = k;
         bj.na = P.h_shape[k];
         bj.rr = L.ranks[k + 1];
-        TTP_CUDA_CHECK(launch_bond(bj, n, s));
+        st = run_bond(o, f, bj, w, n, s);
+        if (st != TTP_OK) return st;
       }
       FiberJob f{};
       f.mode = 1;
@@ -501,15 +556,26 @@ extern "C" int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const doubl
   bj.pairwise = 1;
   bj.sel_stride = cols;
   bj.write_mode = 0;
-  {
+  TTP_CUDA_CHECK(cudaMemsetAsync(bj.status, 0, sizeof(int) * n_mat, s));
+  const int C = force_v0() ? 0 : pick_cluster_size((int)rows, cols, smem_optin_limit());
+  ClusterJob cj{};
+  cj.b = bj;
+  cj.cl = C;
+  cj.src_mode = 1;
+  cj.src = reinterpret_cast<const cplx*>(d_mats);
+  cj.src_stride = mr;
+  cj.Qg = bj.A;
+  cj.q_stride = mr;
+  if (C > 0 && max_active_clusters(cj) > 0) {
+    TTP_CUDA_CHECK(launch_cluster_bond(cj, n_mat, s));
+  } else {
     dim3 grid((unsigned)((mr + 255) / 256), (unsigned)n_mat);
     {
       LaunchScope _ls(KC_MISC, s);
       to_colmajor_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const cplx*>(d_mats), rows, cols, bj.A, mr);
     }
+    TTP_CUDA_CHECK(launch_bond(bj, n_mat, s));
   }
-  TTP_CUDA_CHECK(cudaMemsetAsync(bj.status, 0, sizeof(int) * n_mat, s));
-  TTP_CUDA_CHECK(launch_bond(bj, n_mat, s));
   std::vector<int> sel((size_t)cols * n_mat), stat(n_mat);
   TTP_CUDA_CHECK(cudaMemcpyAsync(sel.data(), bj.sel_out, sizeof(int) * cols * n_mat, cudaMemcpyDeviceToHost, s));
   TTP_CUDA_CHECK(cudaMemcpyAsync(stat.data(), bj.status, sizeof(int) * n_mat, cudaMemcpyDeviceToHost, s));

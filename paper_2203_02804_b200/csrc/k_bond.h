@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include "ttp_common.cuh"
+#include "ttp_internal.h"
 
 #define BOND_THREADS 512
 
@@ -43,3 +44,24 @@ struct BondJob {
 
 size_t bond_smem_bytes(int r);
 cudaError_t launch_bond(const BondJob& job, int n_inst, cudaStream_t s);
+
+// Cluster variant (k_cluster.cu): one thread-block cluster per instance, the
+// block resident in distributed shared memory.
+#define CLUSTER_THREADS 384
+
+struct ClusterJob {
+  BondJob b;              // shared fields (A/W/B/iwork/dwork unused)
+  int cl;                 // CTAs per cluster (1, 2, 4, 8, 16)
+  int src_mode;           // 0: evaluate fibers from `oracle`/`fiber`; 1: numpy row-major `src`
+  OracleDev oracle;
+  FiberJob fiber;         // index-set views and geometry (out/ld unused)
+  const cplx* src;
+  long long src_stride;   // complex elements per instance (src_mode 1)
+  cplx* Qg;               // global Q buffer, m x r column-major per instance
+  long long q_stride;
+};
+
+size_t cluster_smem_bytes(int m, int r, int C);
+int pick_cluster_size(int m, int r, size_t smem_limit);  // 0 if no cluster fits
+int max_active_clusters(const ClusterJob& job);
+cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s);

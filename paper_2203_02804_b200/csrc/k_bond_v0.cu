@@ -20,6 +20,7 @@
 // "first maximum" tie-breaks follow the reference's scan order exactly.
 // All reductions are fixed-order (warp xor trees + ordered warp merge).
 #include "ttp_internal.h"
+#include "bond_common.cuh"
 #include "launch.h"
 #include "k_bond.h"
 
@@ -30,8 +31,6 @@ namespace {
 
 constexpr int NT = BOND_THREADS;
 constexpr int NW = NT / 32;
-constexpr double TOL3Z = 1.0536712127723509e-08;  // sqrt(dlamch('E')), dlamch('E') = 2^-53
-constexpr double SAFMIN_RFG = 2.0041683600089728e-292;  // dlamch('S') / dlamch('E')
 
 struct Ctx {
   int m, r;
@@ -90,100 +89,8 @@ __device__ Ssq block_ssq(Ssq s, Ssq* red) {
   return b;
 }
 
-__device__ double dlapy3(double x, double y, double z) {
-  const double xa = fabs(x), ya = fabs(y), za = fabs(z);
-  const double w = fmax(xa, fmax(ya, za));
-  if (w == 0.0) return xa + ya + za;
-  return w * sqrt((xa / w) * (xa / w) + (ya / w) * (ya / w) + (za / w) * (za / w));
-}
-
-// zlarfg on (alpha, x) given xnorm = ||x||; returns tau, beta and the factor
-// by which x must be scaled (x *= scal * rsafmn^knt).  rescale_pow counts
-// the safmin rescaling rounds (LAPACK loop); rare, handled by the caller.
-struct Reflector {
-  cplx tau;
-  double beta;
-  cplx scal;
-  int knt;
-};
-
-__device__ Reflector zlarfg_core(cplx alpha, double xnorm) {
-  Reflector h;
-  h.knt = 0;
-  double alphr = alpha.x, alphi = alpha.y;
-  if (xnorm == 0.0 && alphi == 0.0) {
-    h.tau = mk(0.0, 0.0);
-    h.beta = alphr;
-    h.scal = mk(1.0, 0.0);
-    return h;
-  }
-  double beta = -copysign(dlapy3(alphr, alphi, xnorm), alphr);
-  const double rsafmn = 1.0 / SAFMIN_RFG;
-  while (fabs(beta) < SAFMIN_RFG && h.knt < 20) {
-    ++h.knt;
-    beta *= rsafmn;
-    alphi *= rsafmn;
-    alphr *= rsafmn;
-    xnorm *= rsafmn;  // caller rescales x; the recomputed norm equals this up to rounding
-  }
-  if (h.knt > 0) beta = -copysign(dlapy3(alphr, alphi, xnorm), alphr);
-  h.tau = mk((beta - alphr) / beta, -alphi / beta);
-  h.scal = cdiv(mk(1.0, 0.0), mk(alphr - beta, alphi));
-  for (int j = 0; j < h.knt; ++j) beta *= SAFMIN_RFG;
-  h.beta = beta;
-  return h;
-}
-
 // ------------------------------------------- small dense LA in shared memory
-// Gauss-Jordan with LAPACK's partial pivoting rule (izamax: |Re|+|Im|,
-// first maximum) on aug = [S | I] (r x 2r, row stride 2r).  On return the
-// right half holds S^-1 and the return value is log|det S| (slogdet); a zero
-// pivot gives -inf.  Every thread returns the same value.
-__device__ double gauss_jordan(const Ctx& c, int r) {
-  cplx* M = c.aug;
-  const int ld = 2 * r;
-  double logdet = 0.0;
-  for (int k = 0; k < r; ++k) {
-    if (threadIdx.x < 32) {
-      ArgMax a{-1.0, LLONG_MAX};
-      for (int i = k + (int)threadIdx.x; i < r; i += 32) {
-        const double v = cabs1(M[i * ld + k]);
-        if (argmax_better(v, i, a.v, a.key)) a = ArgMax{v, i};
-      }
-      a = warp_argmax(a);
-      if (threadIdx.x == 0) c.ibc[0] = (int)a.key;
-    }
-    __syncthreads();
-    const int p = c.ibc[0];
-    if (p != k) {
-      for (int j = threadIdx.x; j < ld; j += NT) {
-        const cplx t = M[k * ld + j];
-        M[k * ld + j] = M[p * ld + j];
-        M[p * ld + j] = t;
-      }
-    }
-    __syncthreads();
-    const cplx piv = M[k * ld + k];
-    const double apiv = cabsh(piv);
-    logdet += log(apiv);
-    if (apiv == 0.0) {
-      __syncthreads();
-      continue;
-    }
-    const cplx rp = cdiv(mk(1.0, 0.0), piv);
-    // save column k multipliers before the pivot row is rescaled
-    for (int i = threadIdx.x; i < r; i += NT) c.vec[i] = (i == k) ? mk(0.0, 0.0) : M[i * ld + k];
-    __syncthreads();
-    for (int j = threadIdx.x; j < ld; j += NT) M[k * ld + j] = cmul(M[k * ld + j], rp);
-    __syncthreads();
-    for (int e = threadIdx.x; e < r * ld; e += NT) {
-      const int i = e / ld, j = e - i * ld;
-      if (i != k) M[e] = csub(M[e], cmul(c.vec[i], M[k * ld + j]));
-    }
-    __syncthreads();
-  }
-  return logdet;
-}
+__device__ double gauss_jordan(const Ctx& c, int r) { return ::gauss_jordan<NT>(c.aug, r, c.vec, c.ibc); }
 
 // aug <- [Q[rows] | I] with Q in logical column order.
 __device__ void load_aug_from_Q(const Ctx& c, const int* rows) {
@@ -569,59 +476,9 @@ __device__ int pairwise_refine(const Ctx& c, double slack, long long swap_limit,
   return TTP_ERR_MAXVOL_ITER;
 }
 
-// One-sided Jacobi singular values of the r x r matrix in aug's left half
-// (single warp; only used when the Frobenius screen cannot rule out
-// cond2 > 1e12).  Returns sigma_max / sigma_min.
 __device__ double jacobi_cond(const Ctx& c) {
-  const int r = c.r, ld = 2 * r;
-  cplx* M = c.aug;
   __shared__ double res;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int sweep = 0; sweep < 60; ++sweep) {
-      double off = 0.0;
-      for (int p = 0; p < r - 1; ++p) {
-        for (int q = p + 1; q < r; ++q) {
-          double app = 0.0, aqq = 0.0;
-          cplx apq = mk(0.0, 0.0);
-          for (int i = lane; i < r; i += 32) {
-            const cplx x = M[i * ld + p], y = M[i * ld + q];
-            app += cabs2(x);
-            aqq += cabs2(y);
-            apq = cfmac(x, y, apq);
-          }
-          app = warp_sum(app);
-          aqq = warp_sum(aqq);
-          apq = warp_sum(apq);
-          const double g = cabsh(apq);
-          if (g == 0.0 || g <= 1e-17 * sqrt(app * aqq)) continue;
-          off = fmax(off, g / sqrt(app * aqq));
-          const double zeta = (aqq - app) / (2.0 * g);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          const cplx ph = mk(apq.x / g, apq.y / g);  // e^{i arg apq}
-          for (int i = lane; i < r; i += 32) {
-            const cplx x = M[i * ld + p], y = M[i * ld + q];
-            // [x y] <- [x y] [[cs, sn*ph], [-sn*conj(ph), cs]]
-            const cplx yp = cmul(y, cconj(ph));
-            M[i * ld + p] = csub(cscale(x, cs), cscale(yp, sn));
-            M[i * ld + q] = cmul(cadd(cscale(x, sn), cscale(yp, cs)), ph);
-          }
-          __syncwarp();
-        }
-      }
-      if (off <= 1e-15) break;
-    }
-    double smax = 0.0, smin = INFINITY;
-    for (int q = 0; q < r; ++q) {
-      double s = 0.0;
-      for (int i = lane; i < r; i += 32) s += cabs2(M[i * ld + q]);
-      s = sqrt(warp_sum(s));
-      smax = fmax(smax, s);
-      smin = fmin(smin, s);
-    }
-    if (lane == 0) res = (smin == 0.0) ? INFINITY : smax / smin;
-  }
+  if (threadIdx.x < 32) jacobi_cond_warp(c.aug, c.r, &res);
   __syncthreads();
   return res;
 }

