@@ -54,6 +54,27 @@ __device__ __forceinline__ Reflector zlarfg_core(cplx alpha, double xnorm) {
   return h;
 }
 
+// zlarfg from the SQUARED norm of x with one sqrt and two divisions (the
+// LAPACK routine uses dlapy3 + four divisions); falls back to zlarfg_core
+// when any intermediate could leave the safe exponent range.  Same
+// reflector up to rounding.
+__device__ __forceinline__ Reflector zlarfg_fast(cplx alpha, double xnorm2) {
+  const double a2 = alpha.x * alpha.x + alpha.y * alpha.y;
+  const double t2 = a2 + xnorm2;
+  if (!(t2 > 1e-280 && t2 < 1e280) || (xnorm2 == 0.0 && alpha.y == 0.0))
+    return zlarfg_core(alpha, sqrt(xnorm2));
+  Reflector h;
+  h.knt = 0;
+  const double beta = -copysign(sqrt(t2), alpha.x);
+  const double ib = 1.0 / beta;
+  h.tau = mk((beta - alpha.x) * ib, -alpha.y * ib);
+  const double dr = alpha.x - beta;
+  const double id = 1.0 / (dr * dr + alpha.y * alpha.y);
+  h.scal = mk(dr * id, -alpha.y * id);
+  h.beta = beta;
+  return h;
+}
+
 __device__ __forceinline__ cplx reflector_scale(const Reflector& h) {
   cplx s = h.scal;
   for (int q = 0; q < h.knt; ++q) s = cscale(s, 1.0 / SAFMIN_RFG);

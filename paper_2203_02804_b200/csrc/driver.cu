@@ -260,7 +260,7 @@ int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const 
     if (k >= 1) {
       const int ra = L.ranks[k], rb = L.ranks[k + 1], nk = P.h_shape[k];
       const size_t smem = sizeof(cplx) * ra * rb;
-      TTP_CUDA_CHECK(cudaFuncSetAttribute(conv_site_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      TTP_CUDA_CHECK(ensure_max_smem((const void*)conv_site_kernel));
       dim3 grid((unsigned)nk, (unsigned)n);
       {
         LaunchScope _ls(KC_CONV_SITE, s);

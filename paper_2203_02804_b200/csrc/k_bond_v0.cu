@@ -701,7 +701,7 @@ size_t bond_smem_bytes(int r) {
 
 cudaError_t launch_bond(const BondJob& job, int n_inst, cudaStream_t s) {
   const size_t smem = bond_smem_bytes(job.r);
-  cudaError_t e = cudaFuncSetAttribute(bond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_max_smem((const void*)bond_kernel);
   if (e != cudaSuccess) return e;
   {
     LaunchScope _ls(KC_BOND, s);

@@ -47,7 +47,7 @@ __device__ int g_phase_enable;
   } while (0)
 
 // Sub-phase cycle accumulators (cluster rank 0, thread 0 of instance 0).
-__device__ unsigned long long g_sub_clock[8];
+__device__ unsigned long long g_sub_clock[16];
 #define SP_BEGIN(t)                                                             \
   long long t = (g_phase_enable && c.crank == 0 && threadIdx.x == 0 && blockIdx.x < (unsigned)c.C) \
                     ? clock64() : 0
@@ -78,6 +78,13 @@ struct Cand {
   double v;
   long long key;
   int row;
+};
+
+struct __align__(16) WCand {
+  double v;
+  long long key;
+  int row;  // global row, -1 = none
+  int pad;
 };
 
 __device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
@@ -118,6 +125,9 @@ struct CC {
   double* vn2;     // ldw
   int* rpos;       // ldw
   Rec* rec;        // 2 (parity double buffer)
+  WCand* wrec;     // [2][CW] per-warp candidates (warp-granular rounds)
+  cplx* wrow;      // [2][CW][r] per-warp candidate row data
+  cplx* bvec;      // [CW][2r] per-warp private broadcast vectors
   Cand* wcand;     // CW
   Ssq* wss;        // CW
   int* ibc;        // 8
@@ -155,6 +165,9 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c) {
   t.vn2 = (double*)take(sizeof(double) * ldw);
   t.rpos = (int*)take(sizeof(int) * ldw);
   t.rec = (Rec*)take(sizeof(Rec) * 2);
+  t.wrec = (WCand*)take(sizeof(WCand) * 2 * CW);
+  t.wrow = (cplx*)take(sizeof(cplx) * 2 * CW * r);
+  t.bvec = (cplx*)take(sizeof(cplx) * CW * 2 * r);
   t.wcand = (Cand*)take(sizeof(Cand) * CW);
   t.wss = (Ssq*)take(sizeof(Ssq) * CW);
   t.ibc = (int*)take(sizeof(int) * 8);
@@ -165,6 +178,7 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c) {
     c->tau = t.tau; c->betas = t.betas; c->cn1 = t.cn1; c->cn2 = t.cn2; c->colmap = t.colmap;
     c->flags = t.flags; c->first = t.first; c->sel = t.sel; c->best = t.best; c->starts = t.starts;
     c->vn1 = t.vn1; c->vn2 = t.vn2; c->rpos = t.rpos; c->rec = t.rec; c->wcand = t.wcand;
+    c->wrec = t.wrec; c->wrow = t.wrow; c->bvec = t.bvec;
     c->wss = t.wss; c->ibc = t.ibc; c->dbc = t.dbc; c->cbc = t.cbc;
   }
   return off;
@@ -308,11 +322,14 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       if (lane == 0) me->data[j] = mk(s.scale, s.ssq);
     }
     cl.sync();
+    // cn1/cn2 hold SQUARED partial column norms: the zlaqp2 downdate
+    // becomes s1' = max(0, s1 - |a|^2), recompute iff s1' <= tol3z * s2
+    // (division free; the idamax choice is order preserving).
     for (int j = warp; j < r; j += CW) {
-      const double nrm = ssq_norm(rank_ssq(cl, c, par, j));
+      const double n2 = ssq_norm2(rank_ssq(cl, c, par, j));
       if (lane == 0) {
-        c.cn1[j] = nrm;
-        c.cn2[j] = nrm;
+        c.cn1[j] = n2;
+        c.cn2[j] = n2;
         c.colmap[j] = j;
       }
     }
@@ -321,11 +338,13 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
   }
   SP_BEGIN(spt);
   for (int i = 0; i < r; ++i) {
-    if (threadIdx.x == 0) {
-      int p = i;
-      for (int j = i + 1; j < r; ++j)
-        if (c.cn1[j] > c.cn1[p]) p = j;
-      if (p != i) {
+    if (warp == 0) {
+      ArgMax am{-1.0, LLONG_MAX};
+      for (int j = i + lane; j < r; j += 32)
+        if (argmax_better(c.cn1[j], j, am.v, am.key)) am = ArgMax{c.cn1[j], j};
+      am = warp_argmax(am);  // idamax: first maximum
+      const int p = (int)am.key;
+      if (lane == 0 && p != i) {
         const int t = c.colmap[p];
         c.colmap[p] = c.colmap[i];
         c.colmap[i] = t;
@@ -365,51 +384,42 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
     SP(spt, 1);
     cl.sync();
     SP(spt, 2);
-    // cross-rank reductions, one warp per item (identical in every CTA)
-    for (int q = warp; q <= ntr; q += CW) {
-      if (q == 0) {
-        const Ssq s = rank_ssq(cl, c, par, 0);
-        const cplx alpha = rank_sum(cl, c, par, 1);
-        if (lane == 0) {
-          Reflector h = zlarfg_core(alpha, ssq_norm(s));
-          c.tau[i] = h.tau;
-          c.betas[i] = fabs(h.beta);
-          c.cbc[0] = reflector_scale(h);
-          c.dbc[0] = h.beta;
-        }
-      } else {
-        const cplx dq = rank_sum(cl, c, par, 1 + q);
-        const cplx aq = rank_sum(cl, c, par, 1 + r + q);
-        if (lane == 0) {
-          c.vec[q - 1] = dq;
-          c.vec2[q - 1] = aq;
-        }
-      }
-    }
-    __syncthreads();
-    const cplx tau = c.tau[i];
+    // Every warp derives the reflector itself (lanes = cluster ranks, fixed
+    // merge order, identical bits everywhere), then finishes its own items:
+    // no block barrier between the cluster barrier and the update.
+    const Ssq sx = rank_ssq(cl, c, par, 0);
+    const cplx alpha = rank_sum(cl, c, par, 1);
+    const Reflector h = (sx.scale > 1e-140 && sx.scale < 1e140) ? zlarfg_fast(alpha, ssq_norm2(sx))
+                                                                  : zlarfg_core(alpha, ssq_norm(sx));
+    const cplx tau = h.tau;
     const bool ident = is_zero(tau);
-    const cplx scal = c.cbc[0];
-    for (int q = 1 + (int)threadIdx.x; q <= ntr; q += CT) {
-      const cplx dots = c.vec[q - 1], arow = c.vec2[q - 1];
-      // v = [1; x*scal]:  s_j = A[i,j] + conj(scal) * (x^H A[:,j])
-      const cplx sj = cadd(arow, cmulc(scal, dots));
-      const cplx tj = ident ? mk(0.0, 0.0) : cmul(cconj(tau), sj);
-      c.vec[q - 1] = tj;
-      const cplx newrow = csub(arow, tj);
-      c.vec2[q - 1] = newrow;
-      // zlaqp2 partial column-norm downdate (replicated)
-      const int j = i + q;
-      int flag = 0;
-      const double v1 = c.cn1[j];
-      if (v1 != 0.0) {
-        double temp = cabsh(newrow) / v1;
-        temp = fmax(1.0 - temp * temp, 0.0);
-        const double rq = v1 / c.cn2[j];
-        if (temp * rq * rq <= TOL3Z) flag = 1;
-        else c.cn1[j] = v1 * sqrt(temp);
+    const cplx scal = reflector_scale(h);
+    if (threadIdx.x == 0) {
+      c.tau[i] = h.tau;
+      c.betas[i] = fabs(h.beta);
+      c.cbc[0] = scal;
+    }
+    for (int q = 1 + warp; q <= ntr; q += CW) {
+      const cplx dots = rank_sum(cl, c, par, 1 + q);
+      const cplx arow = rank_sum(cl, c, par, 1 + r + q);
+      if (lane == 0) {
+        // v = [1; x*scal]:  s_j = A[i,j] + conj(scal) * (x^H A[:,j])
+        const cplx sj = cadd(arow, cmulc(scal, dots));
+        const cplx tj = ident ? mk(0.0, 0.0) : cmul(cconj(tau), sj);
+        c.vec[q - 1] = tj;
+        const cplx newrow = csub(arow, tj);
+        c.vec2[q - 1] = newrow;
+        // zlaqp2 partial column-norm downdate on squared norms (replicated)
+        const int j = i + q;
+        int flag = 0;
+        const double s1 = c.cn1[j];
+        if (s1 != 0.0) {
+          const double s1n = fmax(s1 - cabs2(newrow), 0.0);
+          if (s1n <= TOL3Z * c.cn2[j]) flag = 1;
+          else c.cn1[j] = s1n;
+        }
+        c.flags[q - 1] = flag;
       }
-      c.flags[q - 1] = flag;
     }
     par ^= 1;
     __syncthreads();
@@ -419,7 +429,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       const int g = lo + l;
       if (g < i) continue;
       if (g == i) {
-        Wl(c, l, ci) = mk(c.dbc[0], 0.0);
+        Wl(c, l, ci) = mk(h.beta, 0.0);
         for (int q = 1; q <= ntr; ++q) Wl(c, l, c.colmap[i + q]) = c.vec2[q - 1];
       } else if (!ident) {
         const cplx x = cmul(Wl(c, l, ci), scal);
@@ -450,9 +460,9 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
         if (!c.flags[q]) continue;
         const Ssq s = rank_ssq(cl, c, par, q);
         if (lane == 0) {
-          const double nrm = (i < m - 1) ? ssq_norm(s) : 0.0;
-          c.cn1[i + 1 + q] = nrm;
-          c.cn2[i + 1 + q] = nrm;
+          const double n2 = (i < m - 1) ? ssq_norm2(s) : 0.0;
+          c.cn1[i + 1 + q] = n2;
+          c.cn2[i + 1 + q] = n2;
         }
       }
       par ^= 1;
@@ -491,24 +501,23 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       }
       par ^= 1;
       __syncthreads();
-      for (int l = threadIdx.x; l < nl; l += CT) {
-        const int g = lo + l;
-        if (g < i) continue;
-        const cplx v = (g == i) ? mk(1.0, 0.0) : Wl(c, l, ci);
-        for (int q = 0; q < ntr; ++q) {
-          cplx& a = Wl(c, l, c.colmap[i + 1 + q]);
-          a = csub(a, cmul(v, c.vec[q]));
-        }
-      }
-      __syncthreads();
     }
+    // apply H(i) to the trailing columns and overwrite column i with
+    // H(i) e_i in one pass per row (each thread owns its rows)
     const cplx mt = cneg(ti);
     for (int l = threadIdx.x; l < nl; l += CT) {
       const int g = lo + l;
       cplx& a = Wl(c, l, ci);
-      if (g > i) a = cmul(a, mt);
-      else if (g == i) a = mk(1.0 - ti.x, -ti.y);
-      else a = mk(0.0, 0.0);
+      if (g < i) {
+        a = mk(0.0, 0.0);
+        continue;
+      }
+      const cplx v = (g == i) ? mk(1.0, 0.0) : a;
+      for (int q = 0; q < ntr; ++q) {
+        cplx& b = Wl(c, l, c.colmap[i + 1 + q]);
+        b = csub(b, cmul(v, c.vec[q]));
+      }
+      a = (g > i) ? cmul(a, mt) : mk(1.0 - ti.x, -ti.y);
     }
     __syncthreads();
   }
@@ -521,160 +530,6 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
   __threadfence();
   __syncthreads();
   return true;
-}
-
-// ------------------------------------------------------------ phase B
-__device__ void start_qrcp_qh(cg::cluster_group& cl, CC& c, int& par) {
-  const int r = c.r, lo = c.row0, nl = c.nrows;
-  for (int l = threadIdx.x; l < nl; l += CT) {
-    for (int t = 0; t < r; ++t) Wl(c, l, t) = cconj(Qrow(c, lo + l)[(long long)t * c.m]);
-    const double nrm = ssq_norm(ssq_of(&Wl(c, l, 0), c.ldw, r));
-    c.vn1[l] = nrm;
-    c.vn2[l] = nrm;
-    c.rpos[l] = lo + l;
-  }
-  for (int t = threadIdx.x; t < r; t += CT) c.first[t] = t;
-  __syncthreads();
-  for (int i = 0; i < r; ++i) {
-    Cand a{-1.0, LLONG_MAX, -1};
-    for (int l = threadIdx.x; l < nl; l += CT)
-      if (c.rpos[l] >= i) {
-        Cand b{c.vn1[l], c.rpos[l], l};
-        if (cand_better(b, a)) a = b;
-      }
-    a = block_cand(a, c.wcand);
-    Rec* me = &c.rec[par];
-    if (threadIdx.x == 0) {
-      me->v = a.v;
-      me->key = a.key;
-      me->row = a.row >= 0 ? lo + a.row : -1;
-    }
-    if (a.row >= 0)
-      for (int t = threadIdx.x; t < r; t += CT) me->data[t] = Wl(c, a.row, t);
-    cl.sync();
-    int wr;
-    const Cand w = cluster_winner(cl, c, par, &wr);
-    const Rec* wrec = cl.map_shared_rank(&c.rec[par], wr);
-    if (threadIdx.x < 32) {
-      // winner's column of Q^H (rows i..r-1) -> reflector, one warp
-      const int ln = threadIdx.x;
-      cplx x0 = mk(0.0, 0.0), x1 = mk(0.0, 0.0);
-      const int t0 = i + 1 + ln, t1 = i + 33 + ln;
-      Ssq s = ssq_init();
-      if (t0 < r) {
-        x0 = wrec->data[t0];
-        ssq_addc(s, x0);
-      }
-      if (t1 < r) {
-        x1 = wrec->data[t1];
-        ssq_addc(s, x1);
-      }
-      s = warp_ssq(s);
-      const cplx alpha = wrec->data[i];
-      Reflector h = zlarfg_core(alpha, ssq_norm(s));
-      const cplx sc = reflector_scale(h);
-      const bool ident = is_zero(h.tau);
-      if (t0 < r) c.vec2[t0] = ident ? x0 : cmul(x0, sc);
-      if (t1 < r) c.vec2[t1] = ident ? x1 : cmul(x1, sc);
-      if (ln == 0) {
-        c.vec2[i] = mk(1.0, 0.0);
-        c.cbc[0] = h.tau;
-        const int B = w.row, pvt = (int)w.key;
-        const int A = c.first[i];
-        c.first[i] = B;
-        if (pvt < r) c.first[pvt] = A;
-        if (A >= lo && A < lo + nl) c.rpos[A - lo] = pvt;
-        if (B >= lo && B < lo + nl) c.rpos[B - lo] = i;
-      }
-    }
-    __syncthreads();
-    par ^= 1;
-    const cplx tc = cconj(c.cbc[0]);
-    const bool last = (i == r - 1);
-    for (int l = threadIdx.x; l < nl; l += CT) {
-      if (c.rpos[l] <= i) continue;
-      cplx sacc = mk(0.0, 0.0);
-      for (int t = i; t < r; ++t) sacc = cfmac(c.vec2[t], Wl(c, l, t), sacc);
-      const cplx tt = cmul(tc, sacc);
-      for (int t = i; t < r; ++t) Wl(c, l, t) = csub(Wl(c, l, t), cmul(c.vec2[t], tt));
-      const double v1 = c.vn1[l];
-      if (v1 != 0.0) {
-        double temp = cabsh(Wl(c, l, i)) / v1;
-        temp = fmax(1.0 - temp * temp, 0.0);
-        const double q = v1 / c.vn2[l];
-        if (temp * q * q <= TOL3Z) {
-          double nrm = 0.0;
-          if (!last) nrm = ssq_norm(ssq_of(&Wl(c, l, i + 1), c.ldw, r - i - 1));
-          c.vn1[l] = nrm;
-          c.vn2[l] = nrm;
-        } else {
-          c.vn1[l] = v1 * sqrt(temp);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  for (int t = threadIdx.x; t < r; t += CT) c.starts[t] = c.first[t];
-  __syncthreads();
-}
-
-// ------------------------------------------------------------ phase C
-__device__ void start_lu(cg::cluster_group& cl, CC& c, int& par) {
-  const int r = c.r, lo = c.row0, nl = c.nrows;
-  Cand a{-1.0, LLONG_MAX, -1};
-  for (int l = threadIdx.x; l < nl; l += CT) {
-    for (int t = 0; t < r; ++t) Wl(c, l, t) = Qrow(c, lo + l)[(long long)t * c.m];
-    c.rpos[l] = lo + l;
-    Cand b{cabs1(Wl(c, l, 0)), lo + l, l};
-    if (cand_better(b, a)) a = b;
-  }
-  for (int t = threadIdx.x; t < r; t += CT) c.first[t] = t;
-  for (int k = 0; k < r; ++k) {
-    a = block_cand(a, c.wcand);
-    Rec* me = &c.rec[par];
-    if (threadIdx.x == 0) {
-      me->v = a.v;
-      me->key = a.key;
-      me->row = a.row >= 0 ? lo + a.row : -1;
-    }
-    if (a.row >= 0)
-      for (int t = threadIdx.x; t < r; t += CT) me->data[t] = Wl(c, a.row, t);
-    cl.sync();
-    int wr;
-    const Cand w = cluster_winner(cl, c, par, &wr);
-    const Rec* wrec = cl.map_shared_rank(&c.rec[par], wr);
-    for (int t = threadIdx.x; t < r; t += CT) c.vec[t] = wrec->data[t];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int B = w.row, pvt = (int)w.key;
-      const int A = c.first[k];
-      c.first[k] = B;
-      if (pvt < r) c.first[pvt] = A;
-      if (A >= lo && A < lo + nl) c.rpos[A - lo] = pvt;
-      if (B >= lo && B < lo + nl) c.rpos[B - lo] = k;
-    }
-    __syncthreads();
-    par ^= 1;
-    const cplx piv = c.vec[k];
-    const bool nz = !is_zero(piv);
-    const cplx rp = nz ? cdiv(mk(1.0, 0.0), piv) : mk(0.0, 0.0);
-    a = Cand{-1.0, LLONG_MAX, -1};
-    for (int l = threadIdx.x; l < nl; l += CT) {
-      const int p = c.rpos[l];
-      if (p <= k) continue;
-      if (nz) {
-        const cplx mult = cmul(Wl(c, l, k), rp);
-        Wl(c, l, k) = mult;
-        for (int t = k + 1; t < r; ++t) Wl(c, l, t) = csub(Wl(c, l, t), cmul(mult, c.vec[t]));
-      }
-      if (k + 1 < r) {
-        Cand b{cabs1(Wl(c, l, k + 1)), p, l};
-        if (cand_better(b, a)) a = b;
-      }
-    }
-  }
-  for (int t = threadIdx.x; t < r; t += CT) c.starts[r + t] = c.first[t];
-  __syncthreads();
 }
 
 // ------------------------------------------------------------ phase D
@@ -726,64 +581,370 @@ __device__ Cand form_B(const CC& c) {
   return a;
 }
 
-__device__ int swap_to_dominance(cg::cluster_group& cl, CC& c, int& par, double slack, long long limit) {
+// ======================================================================
+// Warp-granular rounds.  Every warp publishes its own best candidate and
+// that row's data; after the cluster barrier every warp independently finds
+// the cluster-wide winner among the C*CW records and loads the winning row,
+// so a step needs exactly one barrier (the cluster barrier) and no block
+// barrier.  Per-warp copies of the broadcast vectors live in c.bvec.
+// ======================================================================
+__device__ __forceinline__ void warp_publish(const CC& c, int par, const Cand& a) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WCand* slot = &c.wrec[par * CW + w];
+  if (lane == 0) {
+    slot->v = a.v;
+    slot->key = a.key;
+    slot->row = a.row >= 0 ? c.row0 + a.row : -1;
+  }
+  if (a.row >= 0) {
+    cplx* dst = c.wrow + ((long long)par * CW + w) * c.r;
+    for (int t = lane; t < c.r; t += 32) dst[t] = Wl(c, a.row, t);
+  }
+}
+
+struct Winner {
+  Cand w;
+  int rank, slot;
+};
+
+__device__ __forceinline__ Winner warp_winner(cg::cluster_group& cl, const CC& c, int par) {
+  const int lane = threadIdx.x & 31;
+  const int total = c.C * CW;
+  Cand best{-1.0, LLONG_MAX, -1};
+  int bidx = -1;
+  // issue every remote load first (one DSMEM round trip), then compare
+  constexpr int PER = (16 * CW + 31) / 32;
+  double vv[PER];
+  long long kk[PER];
+  int rw[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = lane + 32 * q;
+    rw[q] = -1;
+    if (e < total) {
+      const int rk = e / CW, sl = e - rk * CW;
+      const WCand* p = cl.map_shared_rank(&c.wrec[par * CW + sl], rk);
+      vv[q] = p->v;
+      kk[q] = p->key;
+      rw[q] = p->row;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const Cand x{vv[q], kk[q], rw[q]};
+    if (x.row >= 0 && (bidx < 0 || cand_better(x, best))) {
+      best = x;
+      bidx = lane + 32 * q;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand b;
+    b.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+    b.key = __shfl_xor_sync(0xffffffffu, best.key, o);
+    b.row = __shfl_xor_sync(0xffffffffu, best.row, o);
+    const int bi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (bi >= 0 && (bidx < 0 || cand_better(b, best))) {
+      best = b;
+      bidx = bi;
+    }
+  }
+  Winner W;
+  W.w = best;
+  W.rank = bidx / CW;
+  W.slot = bidx - W.rank * CW;
+  return W;
+}
+
+// entries t = lane and t = lane + 32 of the winner's published row
+__device__ __forceinline__ void winner_row(cg::cluster_group& cl, const CC& c, int par, const Winner& W,
+                                           cplx& x0, cplx& x1) {
+  const int lane = threadIdx.x & 31;
+  const cplx* src = cl.map_shared_rank(c.wrow + ((long long)par * CW + W.slot) * c.r, W.rank);
+  x0 = (lane < c.r) ? src[lane] : mk(0.0, 0.0);
+  x1 = (lane + 32 < c.r) ? src[lane + 32] : mk(0.0, 0.0);
+}
+
+__device__ __forceinline__ cplx lane_entry(cplx x0, cplx x1, int t) {
+  const cplx s = (t < 32) ? x0 : x1;
+  cplx v;
+  v.x = __shfl_sync(0xffffffffu, s.x, t & 31);
+  v.y = __shfl_sync(0xffffffffu, s.y, t & 31);
+  return v;
+}
+
+__device__ __forceinline__ int lane_first(int f0, int f1, int t) {
+  return __shfl_sync(0xffffffffu, (t < 32) ? f0 : f1, t & 31);
+}
+
+// LAPACK interchange of positions i <-> pvt, tracked by warp 0 in registers
+// (lane t holds first[t], first[t+32]); returns the row A previously at i.
+__device__ __forceinline__ int swap_first(const CC& c, int& f0, int& f1, int i, int B, int pvt) {
+  const int lane = threadIdx.x & 31;
+  const int A = lane_first(f0, f1, i);
+  if (lane == (i & 31)) {
+    if (i < 32) f0 = B;
+    else f1 = B;
+  }
+  if (pvt < c.r && lane == (pvt & 31)) {
+    if (pvt < 32) f0 = A;
+    else f1 = A;
+  }
+  return A;
+}
+
+// Position bookkeeping for the rows this thread owns (after the barrier).
+__device__ __forceinline__ void apply_positions(const CC& c, int i, int A, int B, int pvt) {
+  const int la = A - c.row0, lb = B - c.row0;
+  if (la >= 0 && la < c.nrows && (la % CT) == (int)threadIdx.x) c.rpos[la] = pvt;
+  if (lb >= 0 && lb < c.nrows && (lb % CT) == (int)threadIdx.x) c.rpos[lb] = i;
+}
+
+// ======================================================================
+// Shared-winner rounds: every warp publishes its candidate (no block barrier
+// before the cluster barrier); after it, warp 0 alone reads the C*CW records
+// and the winning row over DSMEM (one remote read per CTA, so the winner's
+// shared-memory port is not flooded), prepares the broadcast vector in local
+// shared memory S = c.vec2, and one block barrier hands it to all warps.
+// ======================================================================
+struct Bcast {
+  int i, A, B, pvt;
+};
+
+__device__ __forceinline__ Bcast read_bcast(const CC& c) {
+  return Bcast{c.ibc[4], c.ibc[5], c.ibc[6], c.ibc[7]};
+}
+
+// ---------------------------------------------------------- phase B
+__device__ void start_qrcp_qh_s(cg::cluster_group& cl, CC& c, int& par) {
   const int r = c.r, lo = c.row0, nl = c.nrows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // vn1/vn2 hold SQUARED partial norms here: zlaqp2's downdate
+  //   temp = max(0, 1 - (|a|/vn1)^2); recompute iff temp*(vn1/vn2)^2 <= tol3z
+  // is exactly  s1' = max(0, s1 - |a|^2); recompute iff s1' <= tol3z * s2,
+  // which needs no division, sqrt or hypot (the argmax is order-preserving).
+  for (int l = threadIdx.x; l < nl; l += CT) {
+    for (int t = 0; t < r; ++t) Wl(c, l, t) = cconj(Qrow(c, lo + l)[(long long)t * c.m]);
+    const double n2 = ssq_norm2(ssq_of(&Wl(c, l, 0), c.ldw, r));
+    c.vn1[l] = n2;
+    c.vn2[l] = n2;
+    c.rpos[l] = lo + l;
+  }
+  int f0 = lane, f1 = lane + 32;  // warp 0 only
+  cplx* S = c.vec2;               // v (reflector) of the previous step
+  SP_BEGIN(spt);
+  for (int i = 0; i <= r; ++i) {
+    Cand a{-1.0, LLONG_MAX, -1};
+    const cplx tc = cconj(c.cbc[1]);
+    for (int l = threadIdx.x; l < nl; l += CT) {
+      const int p = c.rpos[l];
+      if (i > 0 && p > i - 1) {
+        // H(i-1)^H applied to this column of Q^H, then the zlaqp2 norm update
+        const int i0 = i - 1;
+        cplx sacc = mk(0.0, 0.0);
+        for (int t = i0; t < r; ++t) sacc = cfmac(S[t], Wl(c, l, t), sacc);
+        const cplx tt = cmul(tc, sacc);
+        for (int t = i0; t < r; ++t) Wl(c, l, t) = csub(Wl(c, l, t), cmul(S[t], tt));
+        const double s1 = c.vn1[l];
+        if (s1 != 0.0) {
+          const double s1n = fmax(s1 - cabs2(Wl(c, l, i0)), 0.0);
+          if (s1n <= TOL3Z * c.vn2[l]) {
+            const double n2 = (i0 < r - 1) ? ssq_norm2(ssq_of(&Wl(c, l, i0 + 1), c.ldw, r - i0 - 1)) : 0.0;
+            c.vn1[l] = n2;
+            c.vn2[l] = n2;
+          } else {
+            c.vn1[l] = s1n;
+          }
+        }
+      }
+      if (i < r && p >= i) {
+        const Cand b{c.vn1[l], p, l};
+        if (cand_better(b, a)) a = b;
+      }
+    }
+    SP(spt, 8);
+    if (i == r) break;
+    a = warp_cand(a);
+    __syncwarp();
+    warp_publish(c, par, a);
+    SP(spt, 9);
+    cl.sync();
+    SP(spt, 10);
+    if (warp == 0) {
+      const Winner W = warp_winner(cl, c, par);
+      cplx x0, x1;
+      winner_row(cl, c, par, W, x0, x1);
+      SP(spt, 11);
+      double s2 = 0.0;
+      if (lane > i && lane < r) s2 += cabs2(x0);
+      if (lane + 32 > i && lane + 32 < r) s2 += cabs2(x1);
+      s2 = warp_sum(s2);
+      const cplx alpha = lane_entry(x0, x1, i);
+      const Reflector h = zlarfg_fast(alpha, s2);
+      const cplx sc = reflector_scale(h);
+      const bool ident = is_zero(h.tau);
+      if (lane >= i && lane < r) S[lane] = (lane == i) ? mk(1.0, 0.0) : (ident ? x0 : cmul(x0, sc));
+      if (lane + 32 >= i && lane + 32 < r) S[lane + 32] = (lane + 32 == i) ? mk(1.0, 0.0) : (ident ? x1 : cmul(x1, sc));
+      const int A = swap_first(c, f0, f1, i, W.w.row, (int)W.w.key);
+      if (lane == 0) {
+        c.cbc[1] = h.tau;
+        c.ibc[4] = i;
+        c.ibc[5] = A;
+        c.ibc[6] = W.w.row;
+        c.ibc[7] = (int)W.w.key;
+      }
+      SP(spt, 12);
+    }
+    __syncthreads();
+    SP(spt, 13);
+    const Bcast bc = read_bcast(c);
+    apply_positions(c, bc.i, bc.A, bc.B, bc.pvt);
+    par ^= 1;
+  }
+  if (warp == 0) {
+    c.starts[lane] = f0;
+    if (lane + 32 < r) c.starts[lane + 32] = f1;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------- phase C
+__device__ void start_lu_s(cg::cluster_group& cl, CC& c, int& par) {
+  const int r = c.r, lo = c.row0, nl = c.nrows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int l = threadIdx.x; l < nl; l += CT) {
+    for (int t = 0; t < r; ++t) Wl(c, l, t) = Qrow(c, lo + l)[(long long)t * c.m];
+    c.rpos[l] = lo + l;
+  }
+  int f0 = lane, f1 = lane + 32;
+  cplx* S = c.vec2;  // pivot row of the previous step
+  for (int k = 0; k <= r; ++k) {
+    Cand a{-1.0, LLONG_MAX, -1};
+    const cplx rp = c.cbc[1];
+    const bool nz = (k > 0) && !is_zero(rp);
+    for (int l = threadIdx.x; l < nl; l += CT) {
+      const int p = c.rpos[l];
+      if (nz && p > k - 1) {
+        const cplx mult = cmul(Wl(c, l, k - 1), rp);
+        Wl(c, l, k - 1) = mult;
+        for (int t = k; t < r; ++t) Wl(c, l, t) = csub(Wl(c, l, t), cmul(mult, S[t]));
+      }
+      if (k < r && p >= k) {
+        const Cand b{cabs1(Wl(c, l, k)), p, l};
+        if (cand_better(b, a)) a = b;
+      }
+    }
+    if (k == r) break;
+    a = warp_cand(a);
+    __syncwarp();
+    warp_publish(c, par, a);
+    cl.sync();
+    if (warp == 0) {
+      const Winner W = warp_winner(cl, c, par);
+      cplx x0, x1;
+      winner_row(cl, c, par, W, x0, x1);
+      if (lane < r) S[lane] = x0;
+      if (lane + 32 < r) S[lane + 32] = x1;
+      const cplx piv = lane_entry(x0, x1, k);
+      const int A = swap_first(c, f0, f1, k, W.w.row, (int)W.w.key);
+      if (lane == 0) {
+        c.cbc[1] = is_zero(piv) ? mk(0.0, 0.0) : cdiv(mk(1.0, 0.0), piv);
+        c.ibc[4] = k;
+        c.ibc[5] = A;
+        c.ibc[6] = W.w.row;
+        c.ibc[7] = (int)W.w.key;
+      }
+    }
+    __syncthreads();
+    const Bcast bc = read_bcast(c);
+    apply_positions(c, bc.i, bc.A, bc.B, bc.pvt);
+    par ^= 1;
+  }
+  if (warp == 0) {
+    c.starts[r + lane] = f0;
+    if (lane + 32 < r) c.starts[r + lane + 32] = f1;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------- phase D
+__device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, double slack, long long limit) {
+  const int r = c.r, lo = c.row0, nl = c.nrows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  cplx* S = c.vec2;  // [0, r): B[i, :] before the update; [r, 2r): w
   invert_rows(c, c.sel);
   Cand a = form_B(c);
   int status = TTP_ERR_MAXVOL_ITER;
   for (long long it = 0;; ++it) {
-    a = block_cand(a, c.wcand);
-    Rec* me = &c.rec[par];
-    if (threadIdx.x == 0) {
-      me->v = a.v;
-      me->key = a.key;
-      me->row = a.row >= 0 ? lo + a.row : -1;
-    }
-    if (a.row >= 0)
-      for (int t = threadIdx.x; t < r; t += CT) me->data[t] = Wl(c, a.row, t);
+    a = warp_cand(a);
+    __syncwarp();
+    warp_publish(c, par, a);
     cl.sync();
-    int wr;
-    const Cand w = cluster_winner(cl, c, par, &wr);
-    if (it >= limit) break;  // guard exhausted (cross.py:127-139)
-    const Rec* wrec = cl.map_shared_rank(&c.rec[par], wr);
-    const int i = (int)(w.key / r), j = (int)(w.key - (long long)(w.key / r) * r);
-    for (int t = threadIdx.x; t < r; t += CT) c.vec2[t] = wrec->data[t];  // B[i, :] before the update
+    if (warp == 0) {
+      const Winner W = warp_winner(cl, c, par);
+      const int i = W.w.row;
+      const int j = (int)(W.w.key - (long long)i * r);
+      cplx x0, x1;
+      winner_row(cl, c, par, W, x0, x1);
+      const cplx pivot = lane_entry(x0, x1, j);
+      // candidates are ranked by |b|^2; the stopping test uses |b| (hypot, as numpy abs)
+      const int done = (cabsh(pivot) <= 1.0 + slack) ? 1 : 0;
+      if (!done && it < limit) {
+        // w[t] = (B[sel[j], t] - B[i, t]) / pivot: one fma per entry in the update
+        if (lane < r) {
+          S[lane] = x0;
+          S[r + lane] = cdiv(csub(c.selb[j * r + lane], x0), pivot);
+        }
+        if (lane + 32 < r) {
+          S[lane + 32] = x1;
+          S[r + lane + 32] = cdiv(csub(c.selb[j * r + lane + 32], x1), pivot);
+        }
+      }
+      if (lane == 0) {
+        c.ibc[4] = i;
+        c.ibc[5] = j;
+        c.ibc[6] = done;
+      }
+    }
     __syncthreads();
-    const cplx pivot = c.vec2[j];
-    // candidates are ranked by |b|^2; the stopping test uses |b| (numpy abs = hypot)
-    if (cabsh(pivot) <= 1.0 + slack) {
+    const int i = c.ibc[4], j = c.ibc[5], done = c.ibc[6];
+    if (it >= limit) break;  // guard exhausted (cross.py:127-139)
+    if (done) {
       status = TTP_OK;
       break;
     }
-    // w[t] = (B[sel[j], t] - B[i, t]) / pivot, so the update is one fma per entry
-    for (int t = threadIdx.x; t < r; t += CT) c.vec[t] = cdiv(csub(c.selb[j * r + t], c.vec2[t]), pivot);
-    __syncthreads();
     par ^= 1;
+    const cplx* w = S + r;
+    // replicated B[sel, :]: rank-1 update of every row, row j <- updated B[i, :]
+    for (int q = warp; q < r; q += CW) {
+      const cplx bqj = (q == j) ? S[j] : c.selb[q * r + j];
+      const cplx* base = (q == j) ? S : c.selb + q * r;
+      cplx y0 = mk(0.0, 0.0), y1 = mk(0.0, 0.0);
+      if (lane < r) y0 = cfma(bqj, w[lane], base[lane]);
+      if (lane + 32 < r) y1 = cfma(bqj, w[lane + 32], base[lane + 32]);
+      __syncwarp();
+      if (lane < r) c.selb[q * r + lane] = y0;
+      if (lane + 32 < r) c.selb[q * r + lane + 32] = y1;
+    }
+    if (threadIdx.x == 0) c.sel[j] = i;
     a = Cand{-1.0, LLONG_MAX, -1};
     for (int l = threadIdx.x; l < nl; l += CT) {
       const cplx blj = Wl(c, l, j);
       for (int t = 0; t < r; ++t) {
-        const cplx v = cfma(blj, c.vec[t], Wl(c, l, t));
+        const cplx v = cfma(blj, w[t], Wl(c, l, t));
         Wl(c, l, t) = v;
-        Cand b{cabs2(v), (long long)(lo + l) * r + t, l};
+        const Cand b{cabs2(v), (long long)(lo + l) * r + t, l};
         if (cand_better(b, a)) a = b;
       }
     }
-    // replicated B[sel, :]: rank-1 update of every row, then row j <- new B[i, :]
-    for (int q = threadIdx.x; q < r; q += CT) {
-      const cplx bqj = c.selb[q * r + j];
-      for (int t = 0; t < r; ++t) c.selb[q * r + t] = cfma(bqj, c.vec[t], c.selb[q * r + t]);
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < r; t += CT) c.selb[j * r + t] = cfma(c.vec2[j], c.vec[t], c.vec2[t]);
-    if (threadIdx.x == 0) c.sel[j] = i;
-    __syncthreads();
     if ((it + 1) % 64 == 0) {
+      __syncthreads();
       invert_rows(c, c.sel);
       a = form_B(c);
     }
   }
   par ^= 1;
+  __syncthreads();
   if (status == TTP_OK && threadIdx.x == 0) insertion_sort(c.sel, r);
   __syncthreads();
   return status;
@@ -793,7 +954,7 @@ __device__ int swap_to_dominance(cg::cluster_group& cl, CC& c, int& par, double 
 __device__ int pairwise_refine(cg::cluster_group& cl, CC& c, int& par, double slack, long long limit) {
   const int m = c.m, r = c.r;
   for (long long round = 0; round < limit; ++round) {
-    const int st = swap_to_dominance(cl, c, par, slack, limit);
+    const int st = swap_to_dominance_s(cl, c, par, slack, limit);
     if (st != TTP_OK) return st;
     invert_rows(c, c.sel);
     form_B(c);
@@ -866,9 +1027,9 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
     __syncthreads();
   } else {
     PHASE_MARK(2);
-    start_qrcp_qh(cl, c, par);
+    start_qrcp_qh_s(cl, c, par);
     PHASE_MARK(3);
-    start_lu(cl, c, par);
+    start_lu_s(cl, c, par);
     PHASE_MARK(4);
     if (threadIdx.x == 0) {
       insertion_sort(c.starts, r);
@@ -886,7 +1047,7 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
     for (int s = 0; s < nstart; ++s) {
       for (int t = threadIdx.x; t < r; t += CT) c.sel[t] = c.starts[s * r + t];
       __syncthreads();
-      const int st = swap_to_dominance(cl, c, par, job.slack, limit);
+      const int st = swap_to_dominance_s(cl, c, par, job.slack, limit);
       PHASE_MARK(5 + s);
       if (st != TTP_OK) {
         err = st;
@@ -1015,7 +1176,7 @@ int pick_cluster_size(int m, int r, size_t smem_limit) {
 cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s) {
   const int C = job.cl;
   const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C);
-  cudaError_t e = cudaFuncSetAttribute(cluster_bond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_max_smem((const void*)cluster_bond_kernel);
   if (e != cudaSuccess) return e;
   if (C > 8) {
     e = cudaFuncSetAttribute(cluster_bond_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1058,8 +1219,7 @@ int max_active_clusters(const ClusterJob& job) {
 }
 
 int max_active_clusters_query(int C, size_t smem) {
-  if (cudaFuncSetAttribute(cluster_bond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return 0;
+  if (ensure_max_smem((const void*)cluster_bond_kernel) != cudaSuccess) return 0;
   if (C > 8 && cudaFuncSetAttribute(cluster_bond_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
     return 0;
   cudaLaunchConfig_t cfg = {};
@@ -1081,13 +1241,13 @@ int max_active_clusters_query(int C, size_t smem) {
 extern "C" int ttp_debug_phase_clocks(int enable, int64_t* out, int32_t n) {
   const int en = enable ? 1 : 0;
   if (out && n > 0) {
-    long long tmp[24];
+    long long tmp[32];
     if (cudaMemcpyFromSymbol(tmp, g_phase_clock, 16 * sizeof(long long)) != cudaSuccess) return TTP_ERR_CUDA;
-    if (cudaMemcpyFromSymbol(tmp + 16, g_sub_clock, 8 * sizeof(long long)) != cudaSuccess) return TTP_ERR_CUDA;
-    for (int i = 0; i < n && i < 24; ++i) out[i] = tmp[i];
+    if (cudaMemcpyFromSymbol(tmp + 16, g_sub_clock, 16 * sizeof(long long)) != cudaSuccess) return TTP_ERR_CUDA;
+    for (int i = 0; i < n && i < 32; ++i) out[i] = tmp[i];
   }
   if (en) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[16] = {};
     if (cudaMemcpyToSymbol(g_sub_clock, z, sizeof(z)) != cudaSuccess) return TTP_ERR_CUDA;
   }
   if (cudaMemcpyToSymbol(g_phase_enable, &en, sizeof(int)) != cudaSuccess) return TTP_ERR_CUDA;

@@ -173,18 +173,48 @@ __global__ void conv_site_kernel(const cplx* __restrict__ cores, long long strid
     G[e] = src[((long long)a * n + s) * rb + c];
   }
   __syncthreads();
+  // Register tile: a warp advances TS samples at once, lane c owns output
+  // columns c and c+32, so each G element loaded from shared memory feeds TS
+  // complex FMAs and each (broadcast) input element feeds two.  The
+  // accumulation order per output is a = 0..ra-1, as in the reference einsum.
+  constexpr int TS = 4;
   const int g0 = goff[s], g1 = goff[s + 1];
-  const int per = blockDim.x / rb;  // samples per pass
-  const int sub = threadIdx.x / rb, c = threadIdx.x - sub * rb;
-  if (sub >= per) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const cplx* vin = Vin + inst * vstride;
   cplx* vout = Vout + inst * vstride;
-  for (int t = g0 + sub; t < g1; t += per) {
-    const long long j = perm[t];
-    const cplx* row = vin + j * ra;
-    cplx acc = mk(0.0, 0.0);
-    for (int a = 0; a < ra; ++a) acc = cfma(row[a], G[a * rb + c], acc);
-    vout[j * rb + c] = acc;
+  const bool c0 = lane < rb, c1 = lane + 32 < rb;
+  for (int t0 = g0 + warp * TS; t0 < g1; t0 += nw * TS) {
+    const cplx* rows[TS];
+    long long js[TS];
+#pragma unroll
+    for (int q = 0; q < TS; ++q) {
+      const int t = min(t0 + q, g1 - 1);
+      js[q] = perm[t];
+      rows[q] = vin + js[q] * ra;
+    }
+    cplx acc0[TS], acc1[TS];
+#pragma unroll
+    for (int q = 0; q < TS; ++q) {
+      acc0[q] = mk(0.0, 0.0);
+      acc1[q] = mk(0.0, 0.0);
+    }
+    for (int a = 0; a < ra; ++a) {
+      const cplx ga = c0 ? G[a * rb + lane] : mk(0.0, 0.0);
+      const cplx gb = c1 ? G[a * rb + lane + 32] : mk(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < TS; ++q) {
+        const cplx x = __ldg(rows[q] + a);
+        acc0[q] = cfma(x, ga, acc0[q]);
+        acc1[q] = cfma(x, gb, acc1[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < TS; ++q) {
+      if (t0 + q < g1) {
+        if (c0) vout[js[q] * rb + lane] = acc0[q];
+        if (c1) vout[js[q] * rb + lane + 32] = acc1[q];
+      }
+    }
   }
 }
 
@@ -247,7 +277,7 @@ extern "C" int ttp_tt_inner(const ttp_tt_batch* bra, const ttp_tt_batch* ket, do
     maxk = max(maxk, ket->h_bonds[q]);
   }
   const size_t smem = sizeof(cplx) * (size_t)(2 * maxb * maxk);
-  TTP_CUDA_CHECK(cudaFuncSetAttribute(tt_inner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TTP_CUDA_CHECK(ensure_max_smem((const void*)tt_inner_kernel));
   {
     LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);
     tt_inner_kernel<<<bra->n_inst, INNER_THREADS, smem, (cudaStream_t)stream>>>(

@@ -63,6 +63,20 @@ LaunchScope::~LaunchScope() {
   g_pending.push_back(Pending{kind, start, stop});
 }
 
+cudaError_t ensure_max_smem(const void* func) {
+  static std::mutex mu;
+  static std::vector<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const void* f : done)
+    if (f == func) return cudaSuccess;
+  int dev = 0, lim = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  if (e == cudaSuccess) done.push_back(func);
+  return e;
+}
+
 extern "C" int64_t ttp_launch_count(void) { return g_launches.load(); }
 
 extern "C" void ttp_profile_enable(int on) { g_profile.store(on ? 1 : 0); }

@@ -133,6 +133,7 @@ TTP_HD Ssq ssq_merge(Ssq a, Ssq b) {
   return Ssq{b.scale, b.ssq + a.ssq * r * r};
 }
 TTP_HD double ssq_norm(Ssq s) { return s.scale == 0.0 ? 0.0 : s.scale * sqrt(s.ssq); }
+TTP_HD double ssq_norm2(Ssq s) { return s.scale == 0.0 ? 0.0 : (s.scale * s.scale) * s.ssq; }
 // Scaled sum of squares of n complex values without per-element divisions:
 // pass 1 finds the largest component, pass 2 sums squares scaled by an exact
 // power of two.  Same value as the LAPACK-style recurrence up to rounding.

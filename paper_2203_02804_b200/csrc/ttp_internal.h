@@ -12,6 +12,12 @@
 int ttp_record_cuda_error(cudaError_t e);
 int ttp_fail(int status, const std::string& msg);
 
+// Raise a kernel's dynamic shared-memory cap to the device's opt-in limit,
+// once per function.  Setting it per launch to the launch's own size races
+// when two host threads launch the same kernel with different sizes (the
+// phi and vhat crosses run concurrently on two streams).
+cudaError_t ensure_max_smem(const void* func);
+
 // Index-set view used by fiber kernels: row t of set k of instance i is at
 // base + i*set_stride + set_offsets[k] + t*d.
 struct SetView {

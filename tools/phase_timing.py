@@ -21,7 +21,7 @@ for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
     P.tt_cross_batch(ob, shape, cfg, with_reports=False)
     torch.cuda.synchronize()
     lib.ttp_debug_phase_clocks(1, None, 0)
-    out = (ctypes.c_int64 * 24)()
+    out = (ctypes.c_int64 * 32)()
     _lib.profile_reset(); _lib.profile_enable(True)
     t0 = time.perf_counter()
     P.tt_cross_batch(ob, shape, cfg, with_reports=False)
@@ -29,7 +29,7 @@ for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
     wall = time.perf_counter() - t0
     _lib.profile_enable(False)
     st = _lib.profile_read()
-    lib.ttp_debug_phase_clocks(0, out, 24)
+    lib.ttp_debug_phase_clocks(0, out, 32)
     clk = [out[i] for i in range(9)]
     ghz = 1.965
     marks = []
@@ -42,3 +42,6 @@ for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
     sub = ["pivot+recomp", "partials", "clsync", "reduce", "update", "-", "zung2r"]
     print("    colbasis sub-phases (all bonds of the sweep): " + " ".join(
         f"{sub[k]}={out[16 + k] / ghz / 1e3:.1f}us" for k in range(7)), flush=True)
+    sub2 = ["s1.local", "s1.publish", "s1.clsync", "s1.winner", "s1.reflector", "s1.barrier"]
+    print("    start1 sub-phases (all bonds): " + " ".join(
+        f"{sub2[k]}={out[24 + k] / ghz / 1e3:.1f}us" for k in range(6)), flush=True)
