@@ -70,9 +70,13 @@ cudaError_t ensure_max_smem(const void* func) {
   for (const void* f : done)
     if (f == func) return cudaSuccess;
   int dev = 0, lim = 0;
+  cudaFuncAttributes fa;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, func);
+  // the cap applies to dynamic shared memory on top of the static amount
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, lim - (int)fa.sharedSizeBytes);
   if (e == cudaSuccess) done.push_back(func);
   return e;
 }
