@@ -56,18 +56,56 @@ class CrossConfig:
             raise ValueError("oracle_call_budget must be >= 1 when set")
 
 
-@dataclass
 class CrossReport:
-    """Outcome record of a TT-cross run (cross.py:73-100)."""
+    """Outcome record of a TT-cross run (cross.py:73-100).
 
-    converged: bool
-    sweeps_used: int
-    oracle_calls: int
-    conv_check_calls: int
-    final_diff: float
-    compression_ratio: float
-    left_sets: list = field(default=None, repr=False, compare=False)
-    right_sets: list = field(default=None, repr=False, compare=False)
+    Same fields and equality as the reference dataclass (the pivot sets are
+    excluded from comparison).  The pivot sets of a batched run are decoded
+    from the device arrays only when first accessed.
+    """
+
+    _FIELDS = ("converged", "sweeps_used", "oracle_calls", "conv_check_calls", "final_diff",
+               "compression_ratio")
+
+    def __init__(self, converged, sweeps_used, oracle_calls, conv_check_calls, final_diff,
+                 compression_ratio, left_sets=None, right_sets=None):
+        self.converged = converged
+        self.sweeps_used = sweeps_used
+        self.oracle_calls = oracle_calls
+        self.conv_check_calls = conv_check_calls
+        self.final_diff = final_diff
+        self.compression_ratio = compression_ratio
+        self._left = left_sets
+        self._right = right_sets
+
+    @property
+    def left_sets(self):
+        if callable(self._left):
+            self._left = self._left()
+        return self._left
+
+    @left_sets.setter
+    def left_sets(self, value):
+        self._left = value
+
+    @property
+    def right_sets(self):
+        if callable(self._right):
+            self._right = self._right()
+        return self._right
+
+    @right_sets.setter
+    def right_sets(self, value):
+        self._right = value
+
+    def __eq__(self, other):
+        if not isinstance(other, CrossReport):
+            return NotImplemented
+        return all(getattr(self, f) == getattr(other, f) for f in self._FIELDS)
+
+    def __repr__(self):
+        inner = ", ".join(f"{f}={getattr(self, f)!r}" for f in self._FIELDS)
+        return f"CrossReport({inner})"
 
     def to_dict(self):
         return {
@@ -268,13 +306,20 @@ def tt_cross_batch(oracles, shape, cfg, with_reports=True):
     total = math.prod(shape)
     reports = []
     lvalid = h["lvalid"].reshape(n, d + 1)
-    for i in range(n):
+
+    def left_of(i):
         if d == 1:
-            lsets, rsets = [[()], None], [None, [()]]
-        else:
-            lsets = [[()]] + [lay.unpack_set(left_h[i], k, k) if lvalid[i, k] else None
-                              for k in range(1, d)] + [None]
-            rsets = [None] + [lay.unpack_set(right_h[i], k, d - k) for k in range(1, d)] + [[()]]
+            return lambda: [[()], None]
+        return lambda: ([[()]] + [lay.unpack_set(left_h[i], k, k) if lvalid[i, k] else None
+                                  for k in range(1, d)] + [None])
+
+    def right_of(i):
+        if d == 1:
+            return lambda: [None, [()]]
+        return lambda: [None] + [lay.unpack_set(right_h[i], k, d - k) for k in range(1, d)] + [[()]]
+
+    for i in range(n):
+        lsets, rsets = left_of(i), right_of(i)
         reports.append(CrossReport(
             converged=bool(h["conv"][i]),
             sweeps_used=int(h["sweeps"][i]),

@@ -27,6 +27,7 @@ __global__ void conv_site_kernel(const cplx* cores, long long stride, long long 
 __global__ void sample_diff_kernel(const cplx* exact, const cplx* approx, long long m,
                                    long long estride, long long astride, double* out,
                                    const int* active);
+size_t conv_site_smem(int ra, int rb, int threads);
 
 namespace {
 thread_local std::string g_last_error;
@@ -66,7 +67,8 @@ struct CrossWs {
 
 CrossWs carve_cross(const ttp_cross_layout& L, int n_inst, long long M, unsigned char* base) {
   CrossWs w{};
-  const long long mr = L.max_rows * (long long)L.max_rank;
+  // padded so row slices of up to 16 cluster CTAs (ceil(m / C) rows each) fit
+  const long long mr = (L.max_rows + 16) * (long long)L.max_rank;
   w.mat_stride = mr;
   w.v_stride = M * (long long)L.max_rank;
   w.iw_stride = 2 * L.max_rows;
@@ -195,7 +197,18 @@ int bond_path_mode() {
     const char* e = getenv("TTP_BOND_PATH");
     if (e && std::strcmp(e, "v0") == 0) return 1;
     if (e && std::strcmp(e, "cluster") == 0) return 2;
+    if (e && std::strncmp(e, "l2", 2) == 0) return 3;
     return 0;
+  }();
+  return v;
+}
+
+// Cluster size of the global-slice ("l2") mode: TTP_BOND_PATH=l2:C.
+int l2_cluster_size() {
+  static const int v = [] {
+    const char* e = getenv("TTP_BOND_PATH");
+    if (e && std::strncmp(e, "l2:", 3) == 0) return std::max(1, atoi(e + 3));
+    return 8;
   }();
   return v;
 }
@@ -216,6 +229,30 @@ size_t smem_optin_limit() {
 // fits, otherwise the fiber kernel followed by the global-memory bond kernel.
 int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const CrossWs& w, int n,
              cudaStream_t s) {
+  // Measured on B200 (profiles/r01/path_sweep.log, path_sweep2.log): for
+  // blocks of >= 1 MB (cfg4/cfg5) at throughput batch sizes, clusters of 2
+  // CTAs with the row slices L2-resident beat the one-CTA kernel and 16-CTA
+  // shared-memory clusters (more instances in flight per barrier round);
+  // smaller blocks run fastest on the one-CTA kernel.
+  const long long block_bytes = (long long)bj.m * bj.r * (long long)sizeof(cplx);
+  const bool auto_l2 = bond_path_mode() == 0 && block_bytes >= (1LL << 20) && n > 16;
+  if (bond_path_mode() == 3 || auto_l2) {
+    ClusterJob cj{};
+    cj.b = bj;
+    const int want = bond_path_mode() == 3 ? l2_cluster_size() : 2;
+    cj.cl = std::min(want, std::max(1, bj.m / std::max(1, bj.r)));
+    cj.src_mode = 0;
+    cj.oracle = o;
+    cj.fiber = f;
+    cj.Qg = w.A;
+    cj.q_stride = w.mat_stride;
+    cj.Wg = w.W;
+    cj.wg_stride = w.mat_stride;
+    if (max_active_clusters(cj) > 0) {
+      TTP_CUDA_CHECK(launch_cluster_bond(cj, n, s));
+      return TTP_OK;
+    }
+  }
   const int C = force_v0() ? 0 : pick_cluster_size(bj.m, bj.r, smem_optin_limit());
   if (C > 0) {
     ClusterJob cj{};
@@ -259,7 +296,7 @@ int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const 
   for (int k = 0; k < d; ++k) {
     if (k >= 1) {
       const int ra = L.ranks[k], rb = L.ranks[k + 1], nk = P.h_shape[k];
-      const size_t smem = sizeof(cplx) * ra * rb;
+      const size_t smem = conv_site_smem(ra, rb, 256);
       TTP_CUDA_CHECK(ensure_max_smem((const void*)conv_site_kernel));
       dim3 grid((unsigned)nk, (unsigned)n);
       {

@@ -59,9 +59,15 @@ struct ClusterJob {
   long long src_stride;   // complex elements per instance (src_mode 1)
   cplx* Qg;               // global Q buffer, m x r column-major per instance
   long long q_stride;
+  // Global-slice mode: when Wg != nullptr each CTA's row slice lives in
+  // global memory (L2-resident for a bounded number of concurrent clusters)
+  // at Wg + inst*wg_stride + rank*ms*r, and only the small state uses shared
+  // memory, so smaller clusters (more instances in flight) are possible.
+  cplx* Wg;
+  long long wg_stride;
 };
 
-size_t cluster_smem_bytes(int m, int r, int C);
+size_t cluster_smem_bytes(int m, int r, int C, bool global_slice = false);
 int pick_cluster_size(int m, int r, size_t smem_limit);  // 0 if no cluster fits
 int max_active_clusters(const ClusterJob& job);
 cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s);

@@ -138,7 +138,89 @@ struct CC {
 __device__ __forceinline__ cplx& Wl(const CC& c, int l, int t) { return c.Ws[(long long)t * c.ldw + l]; }
 __device__ __forceinline__ const cplx* Qrow(const CC& c, int g) { return c.Qg + g; }  // stride m
 
-__host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c) {
+// ---- row kernels with batched loads -------------------------------------
+// In global-slice mode the row slice is L2-resident; issuing a batch of
+// independent loads before the dependent FMAs keeps KB loads in flight per
+// warp instead of one.  Accumulation order is unchanged (t ascending).
+constexpr int KB = 8;
+
+// sum_t conj(S[t]) * W(l, t), t in [t0, r)
+__device__ __forceinline__ cplx row_dotc(const CC& c, const cplx* S, int l, int t0, int r) {
+  const cplx* p = c.Ws + l;
+  const long long ld = c.ldw;
+  cplx acc = mk(0.0, 0.0);
+  int t = t0;
+  for (; t + KB <= r; t += KB) {
+    cplx x[KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) x[q] = p[(t + q) * ld];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) acc = cfmac(S[t + q], x[q], acc);
+  }
+  for (; t < r; ++t) acc = cfmac(S[t], p[t * ld], acc);
+  return acc;
+}
+
+// W(l, t) -= S[t] * f, t in [t0, r)
+__device__ __forceinline__ void row_sub_scaled(const CC& c, const cplx* S, cplx f, int l, int t0, int r) {
+  cplx* p = c.Ws + l;
+  const long long ld = c.ldw;
+  int t = t0;
+  for (; t + KB <= r; t += KB) {
+    cplx x[KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) x[q] = p[(t + q) * ld];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) p[(t + q) * ld] = csub(x[q], cmul(S[t + q], f));
+  }
+  for (; t < r; ++t) p[t * ld] = csub(p[t * ld], cmul(S[t], f));
+}
+
+// W(l, colmap[j0 + q]) -= v * T[q], q in [0, n)   (column-basis updates)
+__device__ __forceinline__ void row_sub_cols(const CC& c, const int* cols, const cplx* T, cplx v, int l,
+                                             int n) {
+  cplx* p = c.Ws + l;
+  const long long ld = c.ldw;
+  int q = 0;
+  for (; q + KB <= n; q += KB) {
+    cplx x[KB];
+    long long off[KB];
+#pragma unroll
+    for (int u = 0; u < KB; ++u) {
+      off[u] = cols[q + u] * ld;
+      x[u] = p[off[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < KB; ++u) p[off[u]] = csub(x[u], cmul(v, T[q + u]));
+  }
+  for (; q < n; ++q) {
+    cplx& a = p[cols[q] * ld];
+    a = csub(a, cmul(v, T[q]));
+  }
+}
+
+// sum over local rows l = l0, l0+32, ... < nl of conj(W(l, ci)) * W(l, cj)
+__device__ __forceinline__ cplx col_dotc(const CC& c, int ci, int cj, int l0, int nl) {
+  const cplx* a = c.Ws + (long long)ci * c.ldw;
+  const cplx* b = c.Ws + (long long)cj * c.ldw;
+  cplx acc = mk(0.0, 0.0);
+  int l = l0;
+  constexpr int RB = 4;
+  for (; l + 32 * (RB - 1) < nl; l += 32 * RB) {
+    cplx x[RB], y[RB];
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      x[u] = a[l + 32 * u];
+      y[u] = b[l + 32 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < RB; ++u) acc = cfmac(x[u], y[u], acc);
+  }
+  for (; l < nl; l += 32) acc = cfmac(a[l], b[l], acc);
+  return acc;
+}
+
+__host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, bool global_slice = false) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     unsigned char* p = base ? base + off : nullptr;
@@ -146,7 +228,7 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c) {
     return p;
   };
   CC t;
-  t.Ws = (cplx*)take(sizeof(cplx) * (size_t)ldw * r);
+  t.Ws = global_slice ? nullptr : (cplx*)take(sizeof(cplx) * (size_t)ldw * r);
   t.aug = (cplx*)take(sizeof(cplx) * 2 * r * r);
   t.selb = (cplx*)take(sizeof(cplx) * r * r);
   t.vec = (cplx*)take(sizeof(cplx) * r);
@@ -373,7 +455,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       } else {
         const int cj = c.colmap[i + q];
         cplx acc = mk(0.0, 0.0);
-        for (int l = lstart + lane; l < nl; l += 32) acc = cfmac(Wl(c, l, ci), Wl(c, l, cj), acc);
+        acc = col_dotc(c, ci, cj, lstart + lane, nl);
         acc = warp_sum(acc);
         if (lane == 0) {
           me->data[1 + q] = acc;
@@ -434,10 +516,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       } else if (!ident) {
         const cplx x = cmul(Wl(c, l, ci), scal);
         Wl(c, l, ci) = x;
-        for (int q = 1; q <= ntr; ++q) {
-          cplx& a = Wl(c, l, c.colmap[i + q]);
-          a = csub(a, cmul(x, c.vec[q - 1]));
-        }
+        row_sub_cols(c, c.colmap + i + 1, c.vec, x, l, ntr);
       }
     }
     __syncthreads();
@@ -490,7 +569,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       for (int q = warp; q < ntr; q += CW) {
         const int cj = c.colmap[i + 1 + q];
         cplx acc = mk(0.0, 0.0);
-        for (int l = lstart + lane; l < nl; l += 32) acc = cfmac(Wl(c, l, ci), Wl(c, l, cj), acc);
+        acc = col_dotc(c, ci, cj, lstart + lane, nl);
         acc = warp_sum(acc);
         if (lane == 0) me->data[q] = own_i ? cadd(acc, Wl(c, li, cj)) : acc;
       }
@@ -513,10 +592,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
         continue;
       }
       const cplx v = (g == i) ? mk(1.0, 0.0) : a;
-      for (int q = 0; q < ntr; ++q) {
-        cplx& b = Wl(c, l, c.colmap[i + 1 + q]);
-        b = csub(b, cmul(v, c.vec[q]));
-      }
+      row_sub_cols(c, c.colmap + i + 1, c.vec, v, l, ntr);
       a = (g > i) ? cmul(a, mt) : mk(1.0 - ti.x, -ti.y);
     }
     __syncthreads();
@@ -741,10 +817,9 @@ __device__ void start_qrcp_qh_s(cg::cluster_group& cl, CC& c, int& par) {
       if (i > 0 && p > i - 1) {
         // H(i-1)^H applied to this column of Q^H, then the zlaqp2 norm update
         const int i0 = i - 1;
-        cplx sacc = mk(0.0, 0.0);
-        for (int t = i0; t < r; ++t) sacc = cfmac(S[t], Wl(c, l, t), sacc);
+        const cplx sacc = row_dotc(c, S, l, i0, r);
         const cplx tt = cmul(tc, sacc);
-        for (int t = i0; t < r; ++t) Wl(c, l, t) = csub(Wl(c, l, t), cmul(S[t], tt));
+        row_sub_scaled(c, S, tt, l, i0, r);
         const double s1 = c.vn1[l];
         if (s1 != 0.0) {
           const double s1n = fmax(s1 - cabs2(Wl(c, l, i0)), 0.0);
@@ -827,7 +902,7 @@ __device__ void start_lu_s(cg::cluster_group& cl, CC& c, int& par) {
       if (nz && p > k - 1) {
         const cplx mult = cmul(Wl(c, l, k - 1), rp);
         Wl(c, l, k - 1) = mult;
-        for (int t = k; t < r; ++t) Wl(c, l, t) = csub(Wl(c, l, t), cmul(mult, S[t]));
+        row_sub_scaled(c, S, mult, l, k, r);
       }
       if (k < r && p >= k) {
         const Cand b{cabs1(Wl(c, l, k)), p, l};
@@ -930,9 +1005,24 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
     a = Cand{-1.0, LLONG_MAX, -1};
     for (int l = threadIdx.x; l < nl; l += CT) {
       const cplx blj = Wl(c, l, j);
-      for (int t = 0; t < r; ++t) {
-        const cplx v = cfma(blj, w[t], Wl(c, l, t));
-        Wl(c, l, t) = v;
+      cplx* p = c.Ws + l;
+      const long long ld = c.ldw;
+      int t = 0;
+      for (; t + KB <= r; t += KB) {
+        cplx x[KB];
+#pragma unroll
+        for (int q = 0; q < KB; ++q) x[q] = p[(t + q) * ld];
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+          const cplx v = cfma(blj, w[t + q], x[q]);
+          p[(t + q) * ld] = v;
+          const Cand b{cabs2(v), (long long)(lo + l) * r + t + q, l};
+          if (cand_better(b, a)) a = b;
+        }
+      }
+      for (; t < r; ++t) {
+        const cplx v = cfma(blj, w[t], p[t * ld]);
+        p[t * ld] = v;
         const Cand b{cabs2(v), (long long)(lo + l) * r + t, l};
         if (cand_better(b, a)) a = b;
       }
@@ -1009,7 +1099,8 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
   c.nrows = max(0, min(job.m, c.row0 + ms) - c.row0);
   c.ldw = ms;
   c.Qg = J.Qg + inst * J.q_stride;
-  carve(smem_raw, ms, job.r, &c);
+  carve(smem_raw, ms, job.r, &c, J.Wg != nullptr);
+  if (J.Wg) c.Ws = J.Wg + inst * J.wg_stride + (long long)c.crank * ms * job.r;
   int par = 0;
   const int r = c.r, m = c.m;
 
@@ -1159,9 +1250,9 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
 
 int max_active_clusters_query(int C, size_t smem);
 
-size_t cluster_smem_bytes(int m, int r, int C) {
+size_t cluster_smem_bytes(int m, int r, int C, bool global_slice) {
   const int ms = (m + C - 1) / C;
-  return carve(nullptr, ms, r, nullptr);
+  return carve(nullptr, ms, r, nullptr, global_slice);
 }
 
 int pick_cluster_size(int m, int r, size_t smem_limit) {
@@ -1175,7 +1266,7 @@ int pick_cluster_size(int m, int r, size_t smem_limit) {
 
 cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s) {
   const int C = job.cl;
-  const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C);
+  const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr);
   cudaError_t e = ensure_max_smem((const void*)cluster_bond_kernel);
   if (e != cudaSuccess) return e;
   if (C > 8) {
@@ -1204,7 +1295,7 @@ cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t 
 
 int max_active_clusters(const ClusterJob& job) {
   const int C = job.cl;
-  const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C);
+  const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr);
   static std::mutex mu;
   static std::map<std::pair<int, size_t>, int> cache;
   {

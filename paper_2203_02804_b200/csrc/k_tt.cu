@@ -172,26 +172,28 @@ __global__ void conv_site_kernel(const cplx* __restrict__ cores, long long strid
     const int a = e / rb, c = e - a * rb;
     G[e] = src[((long long)a * n + s) * rb + c];
   }
-  __syncthreads();
   // Register tile: a warp advances TS samples at once, lane c owns output
-  // columns c and c+32, so each G element loaded from shared memory feeds TS
-  // complex FMAs and each (broadcast) input element feeds two.  The
-  // accumulation order per output is a = 0..ra-1, as in the reference einsum.
-  constexpr int TS = 4;
+  // columns c and c+32.  The TS input rows are first staged in the warp's own
+  // shared-memory slot with coalesced 16-byte loads (each row is contiguous),
+  // then every element is a shared-memory broadcast feeding two complex FMAs,
+  // and each G element feeds TS.  Accumulation order per output is
+  // a = 0..ra-1, as in the reference einsum (tensor_train.py:139).
+  constexpr int TS = 8;
+  cplx* stage = G + ra * rb + (threadIdx.x >> 5) * TS * ra;
+  __syncthreads();
   const int g0 = goff[s], g1 = goff[s + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const cplx* vin = Vin + inst * vstride;
   cplx* vout = Vout + inst * vstride;
   const bool c0 = lane < rb, c1 = lane + 32 < rb;
   for (int t0 = g0 + warp * TS; t0 < g1; t0 += nw * TS) {
-    const cplx* rows[TS];
     long long js[TS];
 #pragma unroll
-    for (int q = 0; q < TS; ++q) {
-      const int t = min(t0 + q, g1 - 1);
-      js[q] = perm[t];
-      rows[q] = vin + js[q] * ra;
-    }
+    for (int q = 0; q < TS; ++q) js[q] = perm[min(t0 + q, g1 - 1)];
+#pragma unroll
+    for (int q = 0; q < TS; ++q)
+      for (int a = lane; a < ra; a += 32) stage[q * ra + a] = __ldg(vin + js[q] * ra + a);
+    __syncwarp();
     cplx acc0[TS], acc1[TS];
 #pragma unroll
     for (int q = 0; q < TS; ++q) {
@@ -203,11 +205,12 @@ __global__ void conv_site_kernel(const cplx* __restrict__ cores, long long strid
       const cplx gb = c1 ? G[a * rb + lane + 32] : mk(0.0, 0.0);
 #pragma unroll
       for (int q = 0; q < TS; ++q) {
-        const cplx x = __ldg(rows[q] + a);
+        const cplx x = stage[q * ra + a];
         acc0[q] = cfma(x, ga, acc0[q]);
         acc1[q] = cfma(x, gb, acc1[q]);
       }
     }
+    __syncwarp();
 #pragma unroll
     for (int q = 0; q < TS; ++q) {
       if (t0 + q < g1) {
@@ -216,6 +219,10 @@ __global__ void conv_site_kernel(const cplx* __restrict__ cores, long long strid
       }
     }
   }
+}
+
+size_t conv_site_smem(int ra, int rb, int threads) {
+  return sizeof(cplx) * ((size_t)ra * rb + (size_t)(threads / 32) * 8 * ra);
 }
 
 // Fixed-order per-instance sums of |exact - approx| and |exact|.

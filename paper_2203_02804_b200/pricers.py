@@ -186,6 +186,10 @@ def run_cross_pair(phi_batch, v_batch, shape, cfg_phi, cfg_v, with_reports=True)
     sweeps overlap on the GPU (each sweep driver blocks its own thread on the
     per-sweep convergence read-back).  Returns (phi_result, v_result)."""
     torch = _lib.require_device()
+    import os
+    if os.environ.get("TTP_PAIR_STREAMS", "1") == "0":  # diagnostics: serialize the two crosses
+        return (tt_cross_batch(phi_batch, shape, cfg_phi, with_reports=with_reports),
+                tt_cross_batch(v_batch, shape, cfg_v, with_reports=with_reports))
     dev = torch.cuda.current_device()
     if dev not in _PAIR_STREAMS:
         _PAIR_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
