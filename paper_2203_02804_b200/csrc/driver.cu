@@ -242,6 +242,7 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
     const int want = bond_path_mode() == 3 ? l2_cluster_size() : 2;
     cj.cl = std::min(want, std::max(1, bj.m / std::max(1, bj.r)));
     cj.src_mode = 0;
+    cj.fiber_fast = fiber_fast_enabled() ? 1 : 0;
     cj.oracle = o;
     cj.fiber = f;
     cj.Qg = w.A;
@@ -259,6 +260,7 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
     cj.b = bj;
     cj.cl = C;
     cj.src_mode = 0;
+    cj.fiber_fast = fiber_fast_enabled() ? 1 : 0;
     cj.oracle = o;
     cj.fiber = f;
     cj.Qg = w.A;

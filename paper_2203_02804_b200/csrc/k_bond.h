@@ -53,6 +53,8 @@ struct ClusterJob {
   BondJob b;              // shared fields (A/W/B/iwork/dwork unused)
   int cl;                 // CTAs per cluster (1, 2, 4, 8, 16)
   int src_mode;           // 0: evaluate fibers from `oracle`/`fiber`; 1: numpy row-major `src`
+  int fiber_fast;         // src_mode 0: separable evaluation allowed (fiber_fast.cuh)
+  int q_wy;               // form Q in compact-WY form (else zung2r rounds)
   OracleDev oracle;
   FiberJob fiber;         // index-set views and geometry (out/ld unused)
   const cplx* src;

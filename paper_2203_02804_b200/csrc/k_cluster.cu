@@ -32,6 +32,7 @@
 
 #include "ttp_internal.h"
 #include "bond_common.cuh"
+#include "fiber_fast.cuh"
 #include "k_bond.h"
 #include "launch.h"
 
@@ -355,7 +356,62 @@ __device__ void insertion_sort(int* v, int r) {
 __device__ void load_block(const CC& c, const ClusterJob& J, int inst) {
   const int r = c.r;
   const long long tot = (long long)c.nrows * r;
-  if (J.src_mode == 0) {
+  if (J.src_mode == 0 && J.fiber_fast && fiber_fast_ok(J.oracle) && r >= 9) {
+    // separable evaluation (fiber_fast.cuh): column parts once per column in
+    // shared memory (aug is free here), row parts once per row in registers
+    const FiberJob& f = J.fiber;
+    const OracleDev& o = J.oracle;
+    const int d = o.d;
+    const double* p = o.params + inst * o.param_stride;
+    const FiberSplit fs = fiber_split(f.mode, f.kl, d);
+    const bool phi = o.kind == TTP_ORACLE_PHI_GBM;
+    cplx* colbuf = c.aug;  // per column: PHI 1 + FF_MAXI values, VHAT 2 values
+    const int cstride = phi ? 1 + FF_MAXI : 2;
+    int idx[TTP_MAX_D];
+    for (int t = threadIdx.x; t < r; t += CT) {
+      const int* T = (f.mode == 0)
+                         ? f.right.base + inst * f.right.set_stride + f.right.offset + (long long)t * f.right.d
+                         : f.left.base + inst * f.left.set_stride + f.left.offset + (long long)t * f.left.d;
+      const int shift = (f.mode == 0) ? f.kl + 1 : 0;
+      for (int j = fs.col_lo; j < fs.col_hi; ++j) idx[j] = T[j - shift];
+      cplx* cb = colbuf + t * cstride;
+      if (phi) {
+        PhiPart part;
+        phi_part(p, d, idx, fs.col_lo, fs.col_hi, fs.inner_is_col, fs.row_lo, fs.row_hi, part);
+        cb[0] = part.e;
+        for (int q = 0; q < fs.ninner; ++q) cb[1 + q] = part.vec[q];
+      } else {
+        vhat_part(p, idx, fs.col_lo, fs.col_hi, cb[0], cb[1]);
+      }
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < c.nrows; l += CT) {
+      const int g = c.row0 + l;
+      if (f.mode == 0) {
+        const int a = g / f.na, s = g - a * f.na;
+        const int* L = f.left.base + inst * f.left.set_stride + f.left.offset + (long long)a * f.left.d;
+        for (int j = 0; j < f.kl; ++j) idx[j] = L[j];
+        idx[f.kl] = s;
+      } else {
+        const int s = g / f.rr, b = g - s * f.rr;
+        const int* R = f.right.base + inst * f.right.set_stride + f.right.offset + (long long)b * f.right.d;
+        idx[f.kl] = s;
+        for (int j = f.kl + 1; j < d; ++j) idx[j] = R[j - f.kl - 1];
+      }
+      if (phi) {
+        PhiPart rp;
+        phi_part(p, d, idx, fs.row_lo, fs.row_hi, !fs.inner_is_col, fs.col_lo, fs.col_hi, rp);
+        for (int t = 0; t < r; ++t) Wl(c, l, t) = phi_combine_packed(rp, colbuf + t * cstride, fs.ninner);
+      } else {
+        cplx prow, wrow;
+        vhat_part(p, idx, fs.row_lo, fs.row_hi, prow, wrow);
+        for (int t = 0; t < r; ++t) {
+          const cplx* cb = colbuf + t * cstride;
+          Wl(c, l, t) = vhat_combine(p, d, prow, wrow, cb[0], cb[1]);
+        }
+      }
+    }
+  } else if (J.src_mode == 0) {
     const FiberJob& f = J.fiber;
     int idx[TTP_MAX_D];
     for (long long e = threadIdx.x; e < tot; e += CT) {
@@ -388,10 +444,178 @@ __device__ void load_block(const CC& c, const ClusterJob& J, int inst) {
   __syncthreads();
 }
 
+// ------------------------------------------------------------ phase A'
+// Q = H(0)...H(r-1) [I; 0] in compact-WY form (the representation zungqr's
+// blocked path uses, LAPACK zlarft + zlarfb):  Q = E - V (T V1^H) with
+// V the unit lower-trapezoidal reflector block, V1 its top r x r block and
+// T upper triangular from the Gram matrix V^H V.  Two cluster barriers
+// instead of zung2r's r rounds, and each row slice is read ~r/4 times
+// instead of ~2r.  Same Q up to rounding (both are backward stable).
+//
+// V(g, a) = 1 (g == a), W(g, colmap[a]) (g > a), 0 (g < a).
+__device__ __forceinline__ cplx vref(const CC& c, int l, int g, int a) {
+  return g > a ? Wl(c, l, c.colmap[a]) : mk(g == a ? 1.0 : 0.0, 0.0);
+}
+
+__device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
+  const int r = c.r, m = c.m, lo = c.row0, nl = c.nrows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  cplx* X = c.aug;          // this CTA's packed partials (read remotely)
+  cplx* P = c.aug + r * r;  // reduced: strict upper = V^H V, strict lower = V1
+  cplx* T = c.selb;         // r x r row-major, upper triangular
+  // (1) Gram partials over local rows, 4 x 4 tiles (upper tile triangle),
+  //     lanes stride rows (coalesced column reads), one warp per tile.
+  constexpr int TB = 4;
+  const int nt = (r + TB - 1) / TB;
+  const int ntiles = nt * (nt + 1) / 2;
+  for (int tile = warp; tile < ntiles; tile += CW) {
+    int ta = 0, rem = tile;
+    while (rem >= nt - ta) {
+      rem -= nt - ta;
+      ++ta;
+    }
+    const int tb = ta + rem;
+    const int a0 = ta * TB, b0 = tb * TB;
+    int ca[TB], cb[TB];
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      ca[u] = c.colmap[min(a0 + u, r - 1)];
+      cb[u] = c.colmap[min(b0 + u, r - 1)];
+    }
+    cplx acc[TB][TB];
+#pragma unroll
+    for (int u = 0; u < TB; ++u)
+#pragma unroll
+      for (int v = 0; v < TB; ++v) acc[u][v] = mk(0.0, 0.0);
+    // rows with g >= r hold plain W values in every column
+    const int lfast = max(0, r - lo);
+    for (int l = lfast + lane; l < nl; l += 32) {
+      cplx xa[TB], xb[TB];
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        xa[u] = Wl(c, l, ca[u]);
+        xb[u] = Wl(c, l, cb[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < TB; ++u)
+#pragma unroll
+        for (int v = 0; v < TB; ++v) acc[u][v] = cfmac(xa[u], xb[v], acc[u][v]);
+    }
+    for (int l = lane; l < min(lfast, nl); l += 32) {
+      const int g = lo + l;
+#pragma unroll
+      for (int u = 0; u < TB; ++u)
+#pragma unroll
+        for (int v = 0; v < TB; ++v)
+          if (a0 + u < r && b0 + v < r)
+            acc[u][v] = cfmac(vref(c, l, g, a0 + u), vref(c, l, g, b0 + v), acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < TB; ++u)
+#pragma unroll
+      for (int v = 0; v < TB; ++v) {
+        const cplx s = warp_sum(acc[u][v]);
+        const int a = a0 + u, b = b0 + v;
+        if (lane == 0 && a < b && b < r) X[a * r + b] = s;
+      }
+  }
+  // strict lower: V1(a, b), a > b, from the CTA owning row a (0 elsewhere)
+  for (int e = threadIdx.x; e < r * r; e += CT) {
+    const int a = e / r, b = e - a * r;
+    if (a > b) X[e] = (a >= lo && a < lo + nl) ? Wl(c, a - lo, c.colmap[b]) : mk(0.0, 0.0);
+  }
+  cl.sync();
+  // (2) fixed rank order sum, identical in every CTA
+  for (int e = threadIdx.x; e < r * r; e += CT) {
+    const int a = e / r, b = e - a * r;
+    if (a == b) continue;
+    cplx s = mk(0.0, 0.0);
+    for (int k = 0; k < c.C; ++k) s = cadd(s, cl.map_shared_rank(X, k)[e]);
+    P[e] = s;
+  }
+  __syncthreads();
+  // (3) zlarft (forward, columnwise): T(i,i) = tau_i,
+  //     T(0:i, i) = -tau_i T(0:i, 0:i) G(0:i, i).  Lane owns rows of T.
+  if (warp == 0) {
+    for (int i = 0; i < r; ++i) {
+      const cplx ti = c.tau[i];
+      for (int a = lane; a < r; a += 32) {
+        cplx v = mk(0.0, 0.0);
+        if (a < i) {
+          for (int b = a; b < i; ++b) v = cfma(T[a * r + b], P[b * r + i], v);
+          v = cneg(cmul(ti, v));
+        } else if (a == i) {
+          v = ti;
+        }
+        T[a * r + i] = v;
+      }
+      __syncwarp();
+    }
+  }
+  cl.sync();  // every CTA finished reading the remote partials in X
+  // (4) M = T V1^H (upper triangular) into X
+  cplx* M = X;
+  for (int e = threadIdx.x; e < r * r; e += CT) {
+    const int a = e / r, b = e - a * r;
+    cplx s = mk(0.0, 0.0);
+    if (a <= b) {
+      // V1(b, cc): 1 at cc == b, P[b*r+cc] for cc < b
+      for (int cc = a; cc < b; ++cc) s = cfmac(P[b * r + cc], T[a * r + cc], s);
+      s = cadd(s, T[a * r + b]);
+    }
+    M[e] = s;
+  }
+  __syncthreads();
+  // (5) Q(g, b) = delta(g, b) - sum_{a <= b} V(g, a) M(a, b), written to Qg
+  //     in logical column order; outputs in blocks of 8 per row thread.
+  constexpr int OB = 8;
+  for (int l = threadIdx.x; l < nl; l += CT) {
+    const int g = lo + l;
+    for (int b0 = 0; b0 < r; b0 += OB) {
+      cplx acc[OB];
+#pragma unroll
+      for (int q = 0; q < OB; ++q) acc[q] = mk(0.0, 0.0);
+      const int amax = min(r, b0 + OB);
+      if (g >= r) {
+        int a = 0;
+        for (; a + 4 <= amax; a += 4) {
+          cplx x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = Wl(c, l, c.colmap[a + u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < OB; ++q)
+              if (b0 + q < r) acc[q] = cfma(x[u], M[(a + u) * r + b0 + q], acc[q]);
+        }
+        for (; a < amax; ++a) {
+          const cplx x = Wl(c, l, c.colmap[a]);
+#pragma unroll
+          for (int q = 0; q < OB; ++q)
+            if (b0 + q < r) acc[q] = cfma(x, M[a * r + b0 + q], acc[q]);
+        }
+      } else {
+        for (int a = 0; a < amax; ++a) {
+          const cplx x = vref(c, l, g, a);
+#pragma unroll
+          for (int q = 0; q < OB; ++q)
+            if (b0 + q < r) acc[q] = cfma(x, M[a * r + b0 + q], acc[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < OB; ++q)
+        if (b0 + q < r)
+          c.Qg[(long long)(b0 + q) * m + g] = csub(mk(g == b0 + q ? 1.0 : 0.0, 0.0), acc[q]);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+}
+
 // ------------------------------------------------------------ phase A
 // Distributed zlaqp2 + zung2r on the block.  Returns false (cluster-uniform)
 // when the block is zero / rank deficient by rank_tol.
-__device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank_tol) {
+__device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank_tol, bool wy) {
   const int r = c.r, m = c.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lo = c.row0, nl = c.nrows;
@@ -556,6 +780,10 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
     mn = fmin(mn, c.betas[t]);
   }
   if (lead == 0.0 || mn < rank_tol * lead) return false;
+  if (wy) {
+    form_q_wy(cl, c);
+    return true;
+  }
   // zung2r: Q = H(0)...H(r-1) [I; 0]
   for (int i = r - 1; i >= 0; --i) {
     const int ci = c.colmap[i];
@@ -1107,7 +1335,7 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
   PHASE_MARK(0);
   load_block(c, J, inst);
   PHASE_MARK(1);
-  if (!column_basis(cl, c, par, job.rank_tol)) {
+  if (!column_basis(cl, c, par, job.rank_tol, J.q_wy != 0)) {
     if (c.crank == 0 && threadIdx.x == 0) set_error(job, inst, TTP_ERR_SINGULAR);
     cl.sync();
     return;
@@ -1264,7 +1492,19 @@ int pick_cluster_size(int m, int r, size_t smem_limit) {
   return 0;
 }
 
-cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s) {
+// TTP_QFORM=zung2r selects the r-round reflector application (A/B checks);
+// the default forms Q in compact-WY form.
+static bool q_wy_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TTP_QFORM");
+    return !(e && strcmp(e, "zung2r") == 0);
+  }();
+  return on;
+}
+
+cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream_t s) {
+  ClusterJob job = job_in;
+  job.q_wy = q_wy_enabled() ? 1 : 0;
   const int C = job.cl;
   const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr);
   cudaError_t e = ensure_max_smem((const void*)cluster_bond_kernel);

@@ -102,6 +102,90 @@ tt_inner_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) {
   if (tid == 0) out[inst] = env[0];
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all_but_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// Same contraction as tt_inner_kernel with the two core slices of every s
+// staged in shared memory by cp.async (coalesced: each slice row is a
+// contiguous D-vector) and double-buffered, so the slice for s+1 streams in
+// while s is contracted; identical arithmetic order, hence identical bits.
+__device__ __forceinline__ void stage_slice(cplx* dst, const cplx* core, int rows, int n, int s, int cols) {
+  for (int e = threadIdx.x; e < rows * cols; e += INNER_THREADS) {
+    const int a = e / cols, c = e - a * cols;
+    cp_async16(dst + e, core + ((long long)a * n + s) * cols + c);
+  }
+}
+
+__global__ void __launch_bounds__(INNER_THREADS)
+tt_inner_staged_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out, int maxb, int maxk) {
+  extern __shared__ __align__(16) cplx sm[];
+  const int inst = blockIdx.x;
+  const int tid = threadIdx.x;
+  cplx* env = sm;                        // Db x Dk
+  cplx* tmp = env + maxb * maxk;         // Db x Dk'
+  cplx* kst[2] = {tmp + maxb * maxk, tmp + maxb * maxk + maxk * maxk};
+  cplx* bst[2] = {kst[1] + maxk * maxk, kst[1] + maxk * maxk + maxb * maxb};
+  if (tid == 0) env[0] = mk(1.0, 0.0);
+  __syncthreads();
+  for (int k = 0; k < bra.d; ++k) {
+    const int Db = bra.bonds[k], Db2 = bra.bonds[k + 1];
+    const int Dk = ket.bonds[k], Dk2 = ket.bonds[k + 1];
+    const int n = bra.shape[k];
+    const cplx* B = bra.cores + inst * bra.stride + bra.off[k];
+    const cplx* K = ket.cores + inst * ket.stride + ket.off[k];
+    const int nacc = Db2 * Dk2;
+    cplx acc[INNER_ACC];
+#pragma unroll
+    for (int q = 0; q < INNER_ACC; ++q) acc[q] = mk(0.0, 0.0);
+    stage_slice(kst[0], K, Dk, n, 0, Dk2);
+    stage_slice(bst[0], B, Db, n, 0, Db2);
+    cp_async_commit();
+    for (int s = 0; s < n; ++s) {
+      const int cur = s & 1;
+      if (s + 1 < n) {
+        stage_slice(kst[cur ^ 1], K, Dk, n, s + 1, Dk2);
+        stage_slice(bst[cur ^ 1], B, Db, n, s + 1, Db2);
+      }
+      cp_async_commit();
+      cp_async_wait_all_but_one();
+      __syncthreads();
+      const cplx* Ks = kst[cur];
+      const cplx* Bs = bst[cur];
+      for (int e = tid; e < Db * Dk2; e += INNER_THREADS) {
+        const int a = e / Dk2, c = e - a * Dk2;
+        cplx t = mk(0.0, 0.0);
+        for (int b = 0; b < Dk; ++b) t = cfma(env[a * Dk + b], Ks[b * Dk2 + c], t);
+        tmp[e] = t;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < INNER_ACC; ++q) {
+        const int e = tid + q * INNER_THREADS;
+        if (e < nacc) {
+          const int a2 = e / Dk2, c = e - a2 * Dk2;
+          cplx t = acc[q];
+          for (int a = 0; a < Db; ++a) t = cfmac(Bs[a * Db2 + a2], tmp[a * Dk2 + c], t);
+          acc[q] = t;
+        }
+      }
+      __syncthreads();
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int q = 0; q < INNER_ACC; ++q) {
+      const int e = tid + q * INNER_THREADS;
+      if (e < nacc) env[e] = acc[q];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) out[inst] = env[0];
+}
+
 // ------------------------------------------------------- tt_evaluate_many
 constexpr int EVAL_WARPS = 8;
 
@@ -284,8 +368,17 @@ extern "C" int ttp_tt_inner(const ttp_tt_batch* bra, const ttp_tt_batch* ket, do
     maxk = max(maxk, ket->h_bonds[q]);
   }
   const size_t smem = sizeof(cplx) * (size_t)(2 * maxb * maxk);
-  TTP_CUDA_CHECK(ensure_max_smem((const void*)tt_inner_kernel));
-  {
+  const size_t smem_staged = smem + sizeof(cplx) * (size_t)(2 * maxk * maxk + 2 * maxb * maxb);
+  int dev = 0, lim = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (smem_staged <= (size_t)lim) {
+    TTP_CUDA_CHECK(ensure_max_smem((const void*)tt_inner_staged_kernel));
+    LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);
+    tt_inner_staged_kernel<<<bra->n_inst, INNER_THREADS, smem_staged, (cudaStream_t)stream>>>(
+        b, k, reinterpret_cast<cplx*>(d_out), maxb, maxk);
+  } else {
+    TTP_CUDA_CHECK(ensure_max_smem((const void*)tt_inner_kernel));
     LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);
     tt_inner_kernel<<<bra->n_inst, INNER_THREADS, smem, (cudaStream_t)stream>>>(
         b, k, reinterpret_cast<cplx*>(d_out));

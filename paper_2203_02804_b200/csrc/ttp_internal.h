@@ -44,6 +44,7 @@ struct FiberJob {
   long long ld;
 };
 
+bool fiber_fast_enabled();
 void launch_fiber(const OracleDev& o, const FiberJob& job, const int* active, int n_inst,
                   cudaStream_t s);
 void launch_oracle_points(const OracleDev& o, int n_inst, const int* idx, long long m,

@@ -327,10 +327,13 @@ def test_p4_cfg3_statistics_against_dense():
     print(f"\n  |gpu-dense| median {np.median(err_gpu):.2e} mean {err_gpu.mean():.2e} max {err_gpu.max():.2e}; "
           f"|ref-dense| median {np.median(err_ref):.2e} mean {err_ref.mean():.2e} max {err_ref.max():.2e}; "
           f"|gpu-ref| median {np.median(gap):.2e} max {gap.max():.2e}")
-    # heavy-tailed per-instance errors (a few unconverged trains dominate the
-    # mean on both sides), so compare medians and bound the tail loosely
+    # heavy-tailed per-instance errors: one unconverged train (1 in 32) sets
+    # the mean on either side and which instance it is moves with 1e-16
+    # rounding, so compare median and upper quartile, count the outliers,
+    # and bound the tail loosely
     assert np.median(err_gpu) <= 2.0 * np.median(err_ref) + 1e-5
-    assert err_gpu.mean() <= 2.0 * err_ref.mean() + 1e-5
+    assert np.quantile(err_gpu, 0.75) <= 2.0 * np.quantile(err_ref, 0.75) + 1e-5
+    assert (err_gpu > 1e-2).sum() <= (err_ref > 1e-2).sum() + 2
     assert err_gpu.max() <= 5e-2
     assert np.median(gap) <= 5e-4
 
@@ -390,7 +393,10 @@ def test_full_size_cfg4_batch_properties():
         assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))
         gm = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, spec.grid.n, spec.grid.eta, spec.grid.alpha)
         cpu_diff = O.sample_diff(list(tt.cores), gm.phi_oracle(), cfg.n_conv_samples, cfg.seed)
-        assert abs(cpu_diff - rep.final_diff) <= 1e-9 * max(cpu_diff, 1e-300) + 1e-15
+        # final_diff = |tt - oracle| / |oracle| over the samples: the
+        # numerator is a cancellation, so device-vs-numpy evaluation order
+        # leaves an absolute ~1e-15 (a few ulps of |oracle|) on top
+        assert abs(cpu_diff - rep.final_diff) <= 1e-9 * max(cpu_diff, 1e-300) + 1e-14
         assert abs(P.tt_inner(tt, tt) - O.tt_inner(tt.cores, tt.cores)) <= 1e-12 * abs(O.tt_inner(tt.cores, tt.cores))
 
 
@@ -402,3 +408,21 @@ def test_batch_prices_equal_single_prices():
     for i in (0, 4):
         single = P.price_fourier_tt(models[i], spec.grid, cfg, cfg, dense_reference="never")
         assert single.price == batch[i].price
+
+
+def test_p4_cfg5_single_option_against_reference():
+    """Config 5 (d=20, N=256, D=64) instance 0: the reference priced it in
+    722 s on this container's CPU (tests/golden/make_golden_cfg5.py); the
+    device price must land within the cross's own noise of it and use the
+    same number of sweeps."""
+    import json
+    import os
+    from conftest import GOLDEN
+    ref = json.load(open(os.path.join(GOLDEN, "cfg5_ref.json")))
+    spec = configs.CONFIGS[5]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    res = P.price_fourier_tt(configs.make_model(5, ref["instance"]), spec.grid, cfg, cfg,
+                             dense_reference="never")
+    assert abs(res.price - ref["price"]) <= 1e-3 * abs(ref["price"])
+    assert res.diagnostics["cross_phi"].sweeps_used == ref["cross_phi"]["sweeps_used"]
+    assert res.diagnostics["cross_v"].sweeps_used == ref["cross_v"]["sweeps_used"]
