@@ -28,6 +28,19 @@ __global__ void sample_diff_kernel(const cplx* exact, const cplx* approx, long l
                                    long long estride, long long astride, double* out,
                                    const int* active);
 size_t conv_site_smem(int ra, int rb, int threads);
+int conv_site_dmma_nt(int rb);
+cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long offk, int ra, int n,
+                                  int rb, const int* perm, const int* goff, const cplx* vin, cplx* vout,
+                                  long long vstride, const int* active, int n_inst, cudaStream_t s);
+
+// TTP_CONV_DMMA=0 selects the scalar-FMA site kernel (A/B checks).
+bool conv_dmma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TTP_CONV_DMMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 namespace {
 thread_local std::string g_last_error;
@@ -298,6 +311,15 @@ int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const 
   for (int k = 0; k < d; ++k) {
     if (k >= 1) {
       const int ra = L.ranks[k], rb = L.ranks[k + 1], nk = P.h_shape[k];
+      if (conv_dmma_enabled() && conv_site_dmma_nt(rb) > 0) {
+        LaunchScope _ls(KC_CONV_SITE, s);
+        TTP_CUDA_CHECK(launch_conv_site_dmma(cores, L.core_stride, L.core_offsets[k], ra, nk, rb,
+                                             P.d_conv_perm + (long long)k * M, P.d_conv_off + goff, vin,
+                                             vout, w.v_stride, d_active, n, s));
+        std::swap(vin, vout);
+        goff += P.h_shape[k] + 1;
+        continue;
+      }
       const size_t smem = conv_site_smem(ra, rb, 256);
       TTP_CUDA_CHECK(ensure_max_smem((const void*)conv_site_kernel));
       dim3 grid((unsigned)nk, (unsigned)n);

@@ -309,6 +309,161 @@ size_t conv_site_smem(int ra, int rb, int threads) {
   return sizeof(cplx) * ((size_t)ra * rb + (size_t)(threads / 32) * 8 * ra);
 }
 
+// FP64 tensor-core variant (DMMA, mma.sync m8n8k4 f64: ~37 TFLOP/s on B200
+// against ~18.6 for FFMA-class DFMA).  The complex product Vout = Vin G is
+// the real GEMM  [Re Im](interleaved) x G'  with
+//     G'[2a+p][2c+q] = Re G[a][c]  (p == q),  Im G[a][c] (p=0,q=1),  -Im G[a][c] (p=1,q=0)
+// so the interleaved complex128 rows of V are the A operand as stored and
+// each accumulator pair (c0, c1) is one complex output.  G' fragments are
+// formed from the complex slice on the fly.  Block: 8 warps, 64 samples per
+// tile (4 warp rows x 16), the N' = 2 rb columns split over 2 warp columns,
+// NT 8-wide n-tiles per warp; tiles of gathered rows double-buffered by
+// cp.async.  Summation order differs from the scalar kernel by rounding only.
+constexpr int CD_ROWS = 64;
+constexpr int CD_THREADS = 256;
+
+__host__ __device__ inline int cd_kp(int ra) { return ((2 * ra + 3) & ~3) + 4; }  // padded row stride (doubles)
+
+template <int NT>
+__global__ void __launch_bounds__(CD_THREADS) conv_site_dmma_kernel(
+    const cplx* __restrict__ cores, long long stride, long long offk, int ra, int n, int rb,
+    const int* __restrict__ perm, const int* __restrict__ goff, const cplx* __restrict__ Vin,
+    cplx* __restrict__ Vout, long long vstride, const int* __restrict__ active) {
+  extern __shared__ __align__(16) double cd_smem[];
+  const int inst = blockIdx.y;
+  if (active && !active[inst]) return;
+  const int s = blockIdx.x;
+  const int g0 = goff[s], g1 = goff[s + 1];
+  if (g0 >= g1) return;
+  const int KP = cd_kp(ra);
+  const int K2 = 2 * ra;
+  const int Kpad = (K2 + 3) & ~3;
+  cplx* G = reinterpret_cast<cplx*>(cd_smem);  // ra x rb
+  double* stage0 = cd_smem + 2 * ((ra * rb + 1) & ~1);
+  double* stage1 = stage0 + CD_ROWS * KP;
+  int* rowj = reinterpret_cast<int*>(stage1 + CD_ROWS * KP);  // [2][CD_ROWS]
+  const cplx* src = cores + inst * stride + offk;
+  for (int e = threadIdx.x; e < ra * rb; e += CD_THREADS) {
+    const int a = e / rb, c = e - a * rb;
+    G[e] = src[((long long)a * n + s) * rb + c];
+  }
+  const cplx* vin = Vin + inst * vstride;
+  cplx* vout = Vout + inst * vstride;
+  const int ntile = (g1 - g0 + CD_ROWS - 1) / CD_ROWS;
+  // zero the K padding columns once (never written by cp.async)
+  for (int e = threadIdx.x; e < 2 * CD_ROWS; e += CD_THREADS) {
+    double* st = (e < CD_ROWS) ? stage0 : stage1;
+    const int row = e % CD_ROWS;
+    for (int k = K2; k < Kpad; ++k) st[row * KP + k] = 0.0;
+  }
+  auto issue = [&](int tile, int buf) {
+    double* st = buf ? stage1 : stage0;
+    int* rj = rowj + buf * CD_ROWS;
+    const int t0 = g0 + tile * CD_ROWS;
+    const int chunks = ra;  // 16-byte chunks per row
+    for (int e = threadIdx.x; e < CD_ROWS * chunks; e += CD_THREADS) {
+      const int row = e / chunks, ch = e - row * chunks;
+      const int t = min(t0 + row, g1 - 1);
+      const int j = perm[t];
+      if (ch == 0) rj[row] = (t0 + row < g1) ? j : -1;
+      cp_async16(st + row * KP + 2 * ch, vin + (long long)j * ra + ch);
+    }
+    cp_async_commit();
+  };
+  issue(0, 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp & 3, wc = warp >> 2;
+  const int ncol0 = wc * NT * 8;  // first real column (of N') of this warp
+  for (int tile = 0; tile < ntile; ++tile) {
+    const int buf = tile & 1;
+    if (tile + 1 < ntile) {
+      issue(tile + 1, buf ^ 1);
+      cp_async_wait_all_but_one();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    const double* st = buf ? stage1 : stage0;
+    const int* rj = rowj + buf * CD_ROWS;
+    double acc[2][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    const double* arow0 = st + (wr * 16 + gid) * KP + tig;
+    const double* arow1 = arow0 + 8 * KP;
+    for (int k0 = 0; k0 < Kpad; k0 += 4) {
+      const double a0 = arow0[k0], a1 = arow1[k0];
+      const int k = k0 + tig;
+      const int a = k >> 1, p = k & 1;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int ncol = ncol0 + nt * 8 + gid;
+        const int c = ncol >> 1, q = ncol & 1;
+        double b = 0.0;
+        if (a < ra && c < rb) {
+          const cplx g = G[a * rb + c];
+          b = (p == q) ? g.x : (q ? g.y : -g.y);
+        }
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[0][nt][0]), "+d"(acc[0][nt][1]) : "d"(a0), "d"(b));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[1][nt][0]), "+d"(acc[1][nt][1]) : "d"(a1), "d"(b));
+      }
+    }
+    // c0, c1 = C'[row][2 tig], C'[row][2 tig + 1] = one complex output
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int j = rj[wr * 16 + mt * 8 + gid];
+      if (j < 0) continue;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = (ncol0 + nt * 8 + 2 * tig) >> 1;
+        if (c < rb) vout[(long long)j * rb + c] = mk(acc[mt][nt][0], acc[mt][nt][1]);
+      }
+    }
+    __syncthreads();  // stage buf is refilled two tiles later
+  }
+}
+
+size_t conv_site_dmma_smem(int ra, int rb) {
+  return sizeof(double) * (2 * (size_t)((ra * rb + 1) & ~1) + 2 * (size_t)CD_ROWS * cd_kp(ra)) +
+         sizeof(int) * 2 * CD_ROWS;
+}
+
+// n-tiles per warp for N' = 2 rb split over 2 warp columns: 1, 2, 4 or 8
+int conv_site_dmma_nt(int rb) {
+  const int need = (2 * rb + 15) / 16;
+  return need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : 0;
+}
+
+cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long offk, int ra, int n,
+                                  int rb, const int* perm, const int* goff, const cplx* vin, cplx* vout,
+                                  long long vstride, const int* active, int n_inst, cudaStream_t s) {
+  const int nt = conv_site_dmma_nt(rb);
+  const size_t smem = conv_site_dmma_smem(ra, rb);
+  dim3 grid((unsigned)n, (unsigned)n_inst);
+#define CD_CASE(NT)                                                                               \
+  case NT: {                                                                                      \
+    cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT>);                      \
+    if (e != cudaSuccess) return e;                                                               \
+    conv_site_dmma_kernel<NT><<<grid, CD_THREADS, smem, s>>>(cores, stride, offk, ra, n, rb, perm, \
+                                                              goff, vin, vout, vstride, active);  \
+    break;                                                                                        \
+  }
+  switch (nt) {
+    CD_CASE(1)
+    CD_CASE(2)
+    CD_CASE(4)
+    CD_CASE(8)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef CD_CASE
+  return cudaGetLastError();
+}
+
 // Fixed-order per-instance sums of |exact - approx| and |exact|.
 __global__ void sample_diff_kernel(const cplx* __restrict__ exact, const cplx* __restrict__ approx,
                                    long long m, long long estride, long long astride,
