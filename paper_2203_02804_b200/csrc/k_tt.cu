@@ -314,18 +314,30 @@ size_t conv_site_smem(int ra, int rb, int threads) {
 // the real GEMM  [Re Im](interleaved) x G'  with
 //     G'[2a+p][2c+q] = Re G[a][c]  (p == q),  Im G[a][c] (p=0,q=1),  -Im G[a][c] (p=1,q=0)
 // so the interleaved complex128 rows of V are the A operand as stored and
-// each accumulator pair (c0, c1) is one complex output.  G' fragments are
-// formed from the complex slice on the fly.  Block: 8 warps, 64 samples per
-// tile (4 warp rows x 16), the N' = 2 rb columns split over 2 warp columns,
-// NT 8-wide n-tiles per warp; tiles of gathered rows double-buffered by
-// cp.async.  Summation order differs from the scalar kernel by rounding only.
+// each accumulator pair (c0, c1) is one complex output.  Block: 8 warps as
+// 2 warp rows x 4 warp columns, 64 samples per tile (CD_MT = 4 m-tiles of 8
+// rows per warp), N' = 2 rb split over the 4 warp columns (NT 8-wide n-tiles
+// each); tiles of gathered rows double-buffered by cp.async.  Summation
+// order differs from the scalar kernel by rounding only.
 constexpr int CD_ROWS = 64;
 constexpr int CD_THREADS = 256;
+constexpr int CD_MT = 4;  // m-tiles (8 rows) per warp
 
 __host__ __device__ inline int cd_kp(int ra) { return ((2 * ra + 3) & ~3) + 4; }  // padded row stride (doubles)
 
-template <int NT>
-__global__ void __launch_bounds__(CD_THREADS) conv_site_dmma_kernel(
+// B' fragment of lane (gid, tig) for k-step k0 and n-tile column n0.
+__device__ __forceinline__ double cd_bfrag(const cplx* G, int ra, int rb, int k0, int n0, int gid, int tig) {
+  const int k = k0 + tig, ncol = n0 + gid;
+  const int a = k >> 1, p = k & 1, c = ncol >> 1, q = ncol & 1;
+  if (a >= ra || c >= rb) return 0.0;
+  const cplx g = G[a * rb + c];
+  return (p == q) ? g.x : (q ? g.y : -g.y);
+}
+
+// KS > 0: all KS x NT B' fragments of the warp live in registers (formed
+// once per CTA); KS == 0: formed per k-step from the complex slice.
+template <int NT, int KS>
+__global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
     const cplx* __restrict__ cores, long long stride, long long offk, int ra, int n, int rb,
     const int* __restrict__ perm, const int* __restrict__ goff, const cplx* __restrict__ Vin,
     cplx* __restrict__ Vout, long long vstride, const int* __restrict__ active) {
@@ -342,20 +354,9 @@ __global__ void __launch_bounds__(CD_THREADS) conv_site_dmma_kernel(
   double* stage0 = cd_smem + 2 * ((ra * rb + 1) & ~1);
   double* stage1 = stage0 + CD_ROWS * KP;
   int* rowj = reinterpret_cast<int*>(stage1 + CD_ROWS * KP);  // [2][CD_ROWS]
-  const cplx* src = cores + inst * stride + offk;
-  for (int e = threadIdx.x; e < ra * rb; e += CD_THREADS) {
-    const int a = e / rb, c = e - a * rb;
-    G[e] = src[((long long)a * n + s) * rb + c];
-  }
   const cplx* vin = Vin + inst * vstride;
   cplx* vout = Vout + inst * vstride;
   const int ntile = (g1 - g0 + CD_ROWS - 1) / CD_ROWS;
-  // zero the K padding columns once (never written by cp.async)
-  for (int e = threadIdx.x; e < 2 * CD_ROWS; e += CD_THREADS) {
-    double* st = (e < CD_ROWS) ? stage0 : stage1;
-    const int row = e % CD_ROWS;
-    for (int k = K2; k < Kpad; ++k) st[row * KP + k] = 0.0;
-  }
   auto issue = [&](int tile, int buf) {
     double* st = buf ? stage1 : stage0;
     int* rj = rowj + buf * CD_ROWS;
@@ -370,11 +371,30 @@ __global__ void __launch_bounds__(CD_THREADS) conv_site_dmma_kernel(
     }
     cp_async_commit();
   };
-  issue(0, 0);
+  issue(0, 0);  // first gather overlaps the slice load below
+  const cplx* src = cores + inst * stride + offk;
+  for (int e = threadIdx.x; e < ra * rb; e += CD_THREADS) {
+    const int a = e / rb, c = e - a * rb;
+    G[e] = src[((long long)a * n + s) * rb + c];
+  }
+  // zero the K padding columns once (never written by cp.async)
+  for (int e = threadIdx.x; e < 2 * CD_ROWS; e += CD_THREADS) {
+    double* st = (e < CD_ROWS) ? stage0 : stage1;
+    const int row = e % CD_ROWS;
+    for (int k = K2; k < Kpad; ++k) st[row * KP + k] = 0.0;
+  }
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int wr = warp & 3, wc = warp >> 2;
+  const int wr = warp & 1, wc = warp >> 1;
   const int ncol0 = wc * NT * 8;  // first real column (of N') of this warp
+  double breg[KS > 0 ? KS : 1][NT];
+  if constexpr (KS > 0) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) breg[ks][nt] = cd_bfrag(G, ra, rb, 4 * ks, ncol0 + nt * 8, gid, tig);
+  }
   for (int tile = 0; tile < ntile; ++tile) {
     const int buf = tile & 1;
     if (tile + 1 < ntile) {
@@ -386,36 +406,45 @@ __global__ void __launch_bounds__(CD_THREADS) conv_site_dmma_kernel(
     __syncthreads();
     const double* st = buf ? stage1 : stage0;
     const int* rj = rowj + buf * CD_ROWS;
-    double acc[2][NT][2];
+    double acc[CD_MT][NT][2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < CD_MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    const double* arow0 = st + (wr * 16 + gid) * KP + tig;
-    const double* arow1 = arow0 + 8 * KP;
-    for (int k0 = 0; k0 < Kpad; k0 += 4) {
-      const double a0 = arow0[k0], a1 = arow1[k0];
-      const int k = k0 + tig;
-      const int a = k >> 1, p = k & 1;
+    const double* arow = st + (wr * 8 * CD_MT + gid) * KP + tig;
+    if constexpr (KS > 0) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int ncol = ncol0 + nt * 8 + gid;
-        const int c = ncol >> 1, q = ncol & 1;
-        double b = 0.0;
-        if (a < ra && c < rb) {
-          const cplx g = G[a * rb + c];
-          b = (p == q) ? g.x : (q ? g.y : -g.y);
-        }
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                     : "+d"(acc[0][nt][0]), "+d"(acc[0][nt][1]) : "d"(a0), "d"(b));
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                     : "+d"(acc[1][nt][0]), "+d"(acc[1][nt][1]) : "d"(a1), "d"(b));
+      for (int ks = 0; ks < KS; ++ks) {
+        if (4 * ks >= Kpad) break;  // KS rounds the k-steps up; columns past Kpad are not staged
+        double av[CD_MT];
+#pragma unroll
+        for (int mt = 0; mt < CD_MT; ++mt) av[mt] = arow[mt * 8 * KP + 4 * ks];
+#pragma unroll
+        for (int mt = 0; mt < CD_MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1]) : "d"(av[mt]), "d"(breg[ks][nt]));
+      }
+    } else {
+      for (int k0 = 0; k0 < Kpad; k0 += 4) {
+        double av[CD_MT], bv[NT];
+#pragma unroll
+        for (int mt = 0; mt < CD_MT; ++mt) av[mt] = arow[mt * 8 * KP + k0];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bv[nt] = cd_bfrag(G, ra, rb, k0, ncol0 + nt * 8, gid, tig);
+#pragma unroll
+        for (int mt = 0; mt < CD_MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1]) : "d"(av[mt]), "d"(bv[nt]));
       }
     }
     // c0, c1 = C'[row][2 tig], C'[row][2 tig + 1] = one complex output
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int j = rj[wr * 16 + mt * 8 + gid];
+    for (int mt = 0; mt < CD_MT; ++mt) {
+      const int j = rj[wr * 8 * CD_MT + mt * 8 + gid];
       if (j < 0) continue;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
@@ -432,10 +461,10 @@ size_t conv_site_dmma_smem(int ra, int rb) {
          sizeof(int) * 2 * CD_ROWS;
 }
 
-// n-tiles per warp for N' = 2 rb split over 2 warp columns: 1, 2, 4 or 8
+// n-tiles per warp for N' = 2 rb split over 4 warp columns: 1, 2 or 4
 int conv_site_dmma_nt(int rb) {
-  const int need = (2 * rb + 15) / 16;
-  return need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : 0;
+  const int need = (2 * rb + 31) / 32;
+  return need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 0;
 }
 
 cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long offk, int ra, int n,
@@ -444,19 +473,23 @@ cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long
   const int nt = conv_site_dmma_nt(rb);
   const size_t smem = conv_site_dmma_smem(ra, rb);
   dim3 grid((unsigned)n, (unsigned)n_inst);
-#define CD_CASE(NT)                                                                               \
-  case NT: {                                                                                      \
-    cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT>);                      \
-    if (e != cudaSuccess) return e;                                                               \
-    conv_site_dmma_kernel<NT><<<grid, CD_THREADS, smem, s>>>(cores, stride, offk, ra, n, rb, perm, \
-                                                              goff, vin, vout, vstride, active);  \
-    break;                                                                                        \
+  // register-resident B' when its KS x NT fragments fit in 32 registers
+  const int ks_need = ((2 * ra + 3) & ~3) / 4;
+  const int ks = ks_need <= 4 ? 4 : ks_need <= 8 ? 8 : ks_need <= 16 ? 16 : 0;
+  const int code = nt * 100 + ((ks > 0 && ks * nt <= 32) ? ks : 0);
+#define CD_CASE(NT, KS)                                                                          \
+  case NT * 100 + KS: {                                                                          \
+    cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS>);                 \
+    if (e != cudaSuccess) return e;                                                              \
+    conv_site_dmma_kernel<NT, KS><<<grid, CD_THREADS, smem, s>>>(cores, stride, offk, ra, n, rb, \
+                                                                  perm, goff, vin, vout, vstride, \
+                                                                  active);                       \
+    break;                                                                                       \
   }
-  switch (nt) {
-    CD_CASE(1)
-    CD_CASE(2)
-    CD_CASE(4)
-    CD_CASE(8)
+  switch (code) {
+    CD_CASE(1, 0) CD_CASE(1, 4) CD_CASE(1, 8) CD_CASE(1, 16)
+    CD_CASE(2, 0) CD_CASE(2, 4) CD_CASE(2, 8) CD_CASE(2, 16)
+    CD_CASE(4, 0) CD_CASE(4, 4) CD_CASE(4, 8)
     default:
       return cudaErrorInvalidValue;
   }
