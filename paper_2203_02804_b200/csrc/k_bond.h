@@ -47,7 +47,7 @@ cudaError_t launch_bond(const BondJob& job, int n_inst, cudaStream_t s);
 
 // Cluster variant (k_cluster.cu): one thread-block cluster per instance, the
 // block resident in distributed shared memory.
-#define CLUSTER_THREADS 384
+#define CLUSTER_THREADS 512
 
 struct ClusterJob {
   BondJob b;              // shared fields (A/W/B/iwork/dwork unused)
