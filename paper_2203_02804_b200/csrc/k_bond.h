@@ -55,6 +55,8 @@ struct ClusterJob {
   int src_mode;           // 0: evaluate fibers from `oracle`/`fiber`; 1: numpy row-major `src`
   int fiber_fast;         // src_mode 0: separable evaluation allowed (fiber_fast.cuh)
   int q_wy;               // form Q in compact-WY form (else zung2r rounds)
+  int fused_starts;       // both dominant-row starts in one read-only pass sequence
+  int debug_start;        // dev aid (TTP_DEBUG_START=1|2): return start set 1 or 2
   OracleDev oracle;
   FiberJob fiber;         // index-set views and geometry (out/ld unused)
   const cplx* src;

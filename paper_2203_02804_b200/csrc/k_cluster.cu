@@ -127,6 +127,9 @@ struct CC {
   int* rpos;       // ldw
   Rec* rec;        // 2 (parity double buffer)
   WCand* wrec;     // [2][CW] per-warp candidates (warp-granular rounds)
+  WCand* wrec2;    // [2][CW] second candidate stream (fused starts)
+  int* rpos2;      // ldw: LU positions (fused starts)
+  cplx* sp;        // 8r scratch vectors (fused starts)
   cplx* wrow;      // [2][CW][r] per-warp candidate row data
   cplx* bvec;      // [CW][2r] per-warp private broadcast vectors
   Cand* wcand;     // CW
@@ -249,11 +252,14 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
   t.rpos = (int*)take(sizeof(int) * ldw);
   t.rec = (Rec*)take(sizeof(Rec) * 2);
   t.wrec = (WCand*)take(sizeof(WCand) * 2 * CW);
+  t.wrec2 = (WCand*)take(sizeof(WCand) * 2 * CW);
+  t.rpos2 = (int*)take(sizeof(int) * ldw);
+  t.sp = (cplx*)take(sizeof(cplx) * 8 * r);
   t.wrow = (cplx*)take(sizeof(cplx) * 2 * CW * r);
   t.bvec = (cplx*)take(sizeof(cplx) * CW * 2 * r);
   t.wcand = (Cand*)take(sizeof(Cand) * CW);
   t.wss = (Ssq*)take(sizeof(Ssq) * CW);
-  t.ibc = (int*)take(sizeof(int) * 8);
+  t.ibc = (int*)take(sizeof(int) * 16);
   t.dbc = (double*)take(sizeof(double) * 8);
   t.cbc = (cplx*)take(sizeof(cplx) * 8);
   if (c) {
@@ -262,6 +268,7 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
     c->flags = t.flags; c->first = t.first; c->sel = t.sel; c->best = t.best; c->starts = t.starts;
     c->vn1 = t.vn1; c->vn2 = t.vn2; c->rpos = t.rpos; c->rec = t.rec; c->wcand = t.wcand;
     c->wrec = t.wrec; c->wrow = t.wrow; c->bvec = t.bvec;
+    c->wrec2 = t.wrec2; c->rpos2 = t.rpos2; c->sp = t.sp;
     c->wss = t.wss; c->ibc = t.ibc; c->dbc = t.dbc; c->cbc = t.cbc;
   }
   return off;
@@ -911,9 +918,17 @@ struct Winner {
   int rank, slot;
 };
 
+__device__ __forceinline__ Winner warp_winner_in(cg::cluster_group& cl, WCand* recs, int par);
+
 __device__ __forceinline__ Winner warp_winner(cg::cluster_group& cl, const CC& c, int par) {
+  return warp_winner_in(cl, c.wrec, par);
+}
+
+// C*CW per-warp records of buffer `par` at recs (same offset in every CTA)
+__device__ __forceinline__ Winner warp_winner_in(cg::cluster_group& cl, WCand* recs, int par) {
   const int lane = threadIdx.x & 31;
-  const int total = c.C * CW;
+  const int C = (int)cl.num_blocks();
+  const int total = C * CW;
   Cand best{-1.0, LLONG_MAX, -1};
   int bidx = -1;
   // issue every remote load first (one DSMEM round trip), then compare
@@ -927,7 +942,7 @@ __device__ __forceinline__ Winner warp_winner(cg::cluster_group& cl, const CC& c
     rw[q] = -1;
     if (e < total) {
       const int rk = e / CW, sl = e - rk * CW;
-      const WCand* p = cl.map_shared_rank(&c.wrec[par * CW + sl], rk);
+      const WCand* p = cl.map_shared_rank(&recs[par * CW + sl], rk);
       vv[q] = p->v;
       kk[q] = p->key;
       rw[q] = p->row;
@@ -1170,6 +1185,251 @@ __device__ void start_lu_s(cg::cluster_group& cl, CC& c, int& par) {
   __syncthreads();
 }
 
+// ---------------------------------------------------------- phase B+C fused
+// Both starts of _dominant_rows (cross.py:172-177) in ONE sequence of r
+// rounds that only READ Q:
+//
+//  * QRCP of Q^H (zlaqp2): after i reflectors the transformed column of
+//    row g is  T_i conj(q_g),  T_i = H_{i-1}^H..H_0^H, so the entry step i
+//    downdates with is  (Pi_{i+1} e_i)^H conj(q_g) = conj(sum_c Pi[c,i] q_g[c])
+//    where Pi_i = H_0..H_{i-1} (r x r, shared memory).  The winner's
+//    transformed column (for zlarfg) is Pi_i^H conj(q_p); a recompute
+//    (tol3z) takes the trailing norm of Pi_{i+1}[:, i+1:]^H conj(q_g).
+//  * LU with partial pivoting (zgetrf): the Schur entry of row g at step k
+//    is  s_gk = q_g[k] - q_g[:k] M_k[:, k],  M_k = U_k^-1 U[:k, :]
+//    (k x r, shared memory), updated by one rank-1 step per pivot; the
+//    winner's U row is  q_p[c] - q_p[:k] M_k[:, c].
+//
+// Every round is one pass over the Q rows (no copies, no writes), one
+// cluster barrier for both arg-maxes, and warps 0 / 1 derive the two
+// winners concurrently.  Pivot decisions are those of the two LAPACK
+// factorizations; the entries agree with the rank-1-updated ones to
+// rounding (same argument as the compact-WY Q).
+constexpr int PLD_PAD = 1;  // Pi / M leading dimension r + 1: conflict-free rows and columns
+
+__device__ __forceinline__ int pi_ld(int r) { return r + PLD_PAD; }
+
+__device__ __forceinline__ void load_qrow_lanes(const CC& c, int g, cplx* dst) {
+  const int lane = threadIdx.x & 31;
+  const cplx* q = Qrow(c, g);
+  for (int t = lane; t < c.r; t += 32) dst[t] = q[(long long)t * c.m];
+  __syncwarp();
+}
+
+__device__ void start_pair_s(cg::cluster_group& cl, CC& c, int& par) {
+  const int r = c.r, lo = c.row0, nl = c.nrows, m = c.m;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ld = pi_ld(r);
+  cplx* Pi = c.aug;    // Pi(c, c') at c' * ld + c   (r x (r+1) <= 2 r^2)
+  cplx* Mm = c.selb;   // M(j, c) at j * r + c        (r x r)
+  cplx* u = c.sp;            // [r]  Pi_{i+1}[:, i] for the next downdate
+  cplx* w2 = c.sp + r;       // [r]  M_{k+1}[:, k+1] for the next Schur column
+  cplx* qr1 = c.sp + 2 * r;  // [r]  winner Q rows
+  cplx* qr2 = c.sp + 3 * r;
+  cplx* vv = c.sp + 4 * r;   // [r]  reflector v (entries >= i)
+  cplx* yy = c.sp + 5 * r;   // [r]  Pi v
+  cplx* mrow = c.sp + 6 * r; // [r]  new M row U[k, :] / U[k, k]
+  cplx* mcol = c.sp + 7 * r; // [r]  M_k[:, k]
+  for (int e = threadIdx.x; e < r * ld; e += CT) {
+    const int cc = e / ld, rr = e - cc * ld;
+    Pi[e] = mk((rr == cc) ? 1.0 : 0.0, 0.0);
+  }
+  for (int l = threadIdx.x; l < nl; l += CT) {
+    const double n2 = ssq_norm2(ssq_of(Qrow(c, lo + l), m, r));
+    c.vn1[l] = n2;
+    c.vn2[l] = n2;
+    c.rpos[l] = lo + l;
+    c.rpos2[l] = lo + l;
+  }
+  int f0 = lane, f1 = lane + 32;  // warp 0: QRCP first[]; warp 1: LU first[]
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    // ---- row pass: downdate with step k-1 (QRCP), Schur column k (LU)
+    Cand a1{-1.0, LLONG_MAX, -1}, a2{-1.0, LLONG_MAX, -1};
+    for (int l = threadIdx.x; l < nl; l += CT) {
+      const int p1 = c.rpos[l], p2 = c.rpos2[l];
+      const bool dd = (k > 0 && p1 > k - 1);
+      const bool lu = (p2 >= k);
+      if (!dd && !lu) {
+        if (p1 >= k) {
+          const Cand b{c.vn1[l], p1, l};
+          if (cand_better(b, a1)) a1 = b;
+        }
+        continue;
+      }
+      const cplx* q = Qrow(c, lo + l);
+      cplx t1 = mk(0.0, 0.0), s2 = mk(0.0, 0.0);
+      int t = 0;
+      for (; t + KB <= r; t += KB) {
+        cplx x[KB];
+#pragma unroll
+        for (int qq = 0; qq < KB; ++qq) x[qq] = q[(long long)(t + qq) * m];
+#pragma unroll
+        for (int qq = 0; qq < KB; ++qq) {
+          t1 = cfma(u[t + qq], x[qq], t1);
+          if (t + qq < k) s2 = cfma(x[qq], w2[t + qq], s2);
+          else if (t + qq == k) s2 = csub(x[qq], s2);
+        }
+      }
+      for (; t < r; ++t) {
+        const cplx x = q[(long long)t * m];
+        t1 = cfma(u[t], x, t1);
+        if (t < k) s2 = cfma(x, w2[t], s2);
+        else if (t == k) s2 = csub(x, s2);
+      }
+      if (dd) {
+        const double s1 = c.vn1[l];
+        if (s1 != 0.0) {
+          const double s1n = fmax(s1 - cabs2(t1), 0.0);
+          if (s1n <= TOL3Z * c.vn2[l]) {
+            // trailing norm of the transformed column: entries k .. r-1
+            Ssq s = ssq_init();
+            for (int cc = k; cc < r; ++cc) {
+              cplx e = mk(0.0, 0.0);
+              for (int j = 0; j < r; ++j) e = cfma(Pi[cc * ld + j], q[(long long)j * m], e);
+              ssq_addc(s, e);
+            }
+            const double n2 = (k - 1 < r - 1) ? ssq_norm2(s) : 0.0;
+            c.vn1[l] = n2;
+            c.vn2[l] = n2;
+          } else {
+            c.vn1[l] = s1n;
+          }
+        }
+      }
+      if (p1 >= k) {
+        const Cand b{c.vn1[l], p1, l};
+        if (cand_better(b, a1)) a1 = b;
+      }
+      if (lu) {
+        const Cand b{cabs1(s2), p2, l};
+        if (cand_better(b, a2)) a2 = b;
+      }
+    }
+    a1 = warp_cand(a1);
+    a2 = warp_cand(a2);
+    if (lane == 0) {
+      WCand* s1p = &c.wrec[par * CW + warp];
+      s1p->v = a1.v;
+      s1p->key = a1.key;
+      s1p->row = a1.row >= 0 ? lo + a1.row : -1;
+      WCand* s2p = &c.wrec2[par * CW + warp];
+      s2p->v = a2.v;
+      s2p->key = a2.key;
+      s2p->row = a2.row >= 0 ? lo + a2.row : -1;
+    }
+    cl.sync();
+    if (warp == 0) {
+      // ---- QRCP winner: reflector H_k from Pi_k^H conj(q_p)
+      const Winner W = warp_winner_in(cl, c.wrec, par);
+      load_qrow_lanes(c, W.w.row, qr1);
+      cplx x0 = mk(0.0, 0.0), x1 = mk(0.0, 0.0);
+      for (int cc = lane; cc < r; cc += 32) {
+        cplx e = mk(0.0, 0.0);
+        for (int j = 0; j < r; ++j) e = cfma(Pi[cc * ld + j], qr1[j], e);
+        if (cc < 32) x0 = cconj(e);
+        else x1 = cconj(e);
+      }
+      double sx = 0.0;
+      if (lane > k && lane < r) sx += cabs2(x0);
+      if (lane + 32 > k && lane + 32 < r) sx += cabs2(x1);
+      sx = warp_sum(sx);
+      const cplx alpha = lane_entry(x0, x1, k);
+      const Reflector h = zlarfg_fast(alpha, sx);
+      const cplx sc = reflector_scale(h);
+      const bool ident = is_zero(h.tau);
+      for (int cc = lane; cc < r; cc += 32) {
+        const cplx xv = (cc < 32) ? x0 : x1;
+        vv[cc] = (cc < k) ? mk(0.0, 0.0) : (cc == k) ? mk(1.0, 0.0) : (ident ? xv : cmul(xv, sc));
+      }
+      __syncwarp();
+      // y = Pi v; u = Pi_{k+1}[:, k] = Pi[:, k] - tau y  (v[k] = 1)
+      for (int cc = lane; cc < r; cc += 32) {
+        cplx y = mk(0.0, 0.0);
+        for (int j = k; j < r; ++j) y = cfma(Pi[j * ld + cc], vv[j], y);
+        yy[cc] = y;
+        u[cc] = csub(Pi[k * ld + cc], cmul(h.tau, y));
+      }
+      const int A = swap_first(c, f0, f1, k, W.w.row, (int)W.w.key);
+      if (lane == 0) {
+        c.cbc[1] = h.tau;
+        c.ibc[4] = k;
+        c.ibc[5] = A;
+        c.ibc[6] = W.w.row;
+        c.ibc[7] = (int)W.w.key;
+      }
+    } else if (warp == 1) {
+      // ---- LU winner: U row k, pivot, next Schur multipliers
+      const Winner W = warp_winner_in(cl, c.wrec2, par);
+      load_qrow_lanes(c, W.w.row, qr2);
+      cplx u0 = mk(0.0, 0.0), u1 = mk(0.0, 0.0);
+      for (int cc = lane; cc < r; cc += 32) {
+        cplx e = mk(0.0, 0.0);
+        if (cc >= k) {
+          for (int j = 0; j < k; ++j) e = cfma(qr2[j], Mm[j * r + cc], e);
+          e = csub(qr2[cc], e);
+        }
+        if (cc < 32) u0 = e;
+        else u1 = e;
+      }
+      const cplx piv = lane_entry(u0, u1, k);
+      const bool zp = is_zero(piv);
+      const cplx rp = zp ? mk(0.0, 0.0) : cdiv(mk(1.0, 0.0), piv);
+      for (int cc = lane; cc < r; cc += 32) {
+        const cplx e = (cc < 32) ? u0 : u1;
+        mrow[cc] = (cc < k || zp) ? mk(0.0, 0.0) : (cc == k ? mk(1.0, 0.0) : cmul(e, rp));
+        if (cc < k) mcol[cc] = Mm[cc * r + k];
+      }
+      __syncwarp();
+      // w2 = M_{k+1}[:, k+1]
+      if (k + 1 < r) {
+        for (int j = lane; j <= k; j += 32)
+          w2[j] = (j < k) ? csub(Mm[j * r + k + 1], cmul(mcol[j], mrow[k + 1])) : mrow[k + 1];
+      }
+      const int A = swap_first(c, f0, f1, k, W.w.row, (int)W.w.key);
+      if (lane == 0) {
+        c.ibc[8] = k;
+        c.ibc[9] = A;
+        c.ibc[10] = W.w.row;
+        c.ibc[11] = (int)W.w.key;
+      }
+    }
+    __syncthreads();
+    // ---- replicated bookkeeping and the two small rank-1 updates
+    {
+      const int i = c.ibc[4], A = c.ibc[5], B = c.ibc[6], pvt = c.ibc[7];
+      const int la = A - lo, lb = B - lo;
+      if (la >= 0 && la < nl && (la % CT) == (int)threadIdx.x) c.rpos[la] = pvt;
+      if (lb >= 0 && lb < nl && (lb % CT) == (int)threadIdx.x) c.rpos[lb] = i;
+      const int i2 = c.ibc[8], A2 = c.ibc[9], B2 = c.ibc[10], pvt2 = c.ibc[11];
+      const int la2 = A2 - lo, lb2 = B2 - lo;
+      if (la2 >= 0 && la2 < nl && (la2 % CT) == (int)threadIdx.x) c.rpos2[la2] = pvt2;
+      if (lb2 >= 0 && lb2 < nl && (lb2 % CT) == (int)threadIdx.x) c.rpos2[lb2] = i2;
+    }
+    const cplx tau = c.cbc[1];
+    const int ncol = r - k;
+    for (int e = threadIdx.x; e < r * ncol; e += CT) {
+      const int cp = k + e / r, cc = e - (e / r) * r;  // Pi(cc, cp) -= tau y[cc] conj(v[cp])
+      Pi[cp * ld + cc] = csub(Pi[cp * ld + cc], cmul(cmul(tau, yy[cc]), cconj(vv[cp])));
+    }
+    for (int e = threadIdx.x; e < (k + 1) * ncol; e += CT) {
+      const int j = e / ncol, cc = k + (e - j * ncol);
+      if (j < k) Mm[j * r + cc] = csub(Mm[j * r + cc], cmul(mcol[j], mrow[cc]));
+      else Mm[k * r + cc] = mrow[cc];
+    }
+    par ^= 1;
+    __syncthreads();
+  }
+  if (warp == 0) {
+    if (lane < r) c.starts[lane] = f0;
+    if (lane + 32 < r) c.starts[lane + 32] = f1;
+  } else if (warp == 1) {
+    if (lane < r) c.starts[r + lane] = f0;
+    if (lane + 32 < r) c.starts[r + lane + 32] = f1;
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------- phase D
 __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, double slack, long long limit) {
   const int r = c.r, lo = c.row0, nl = c.nrows;
@@ -1346,9 +1606,14 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
     __syncthreads();
   } else {
     PHASE_MARK(2);
-    start_qrcp_qh_s(cl, c, par);
-    PHASE_MARK(3);
-    start_lu_s(cl, c, par);
+    if (J.fused_starts) {
+      start_pair_s(cl, c, par);
+      PHASE_MARK(3);
+    } else {
+      start_qrcp_qh_s(cl, c, par);
+      PHASE_MARK(3);
+      start_lu_s(cl, c, par);
+    }
     PHASE_MARK(4);
     if (threadIdx.x == 0) {
       insertion_sort(c.starts, r);
@@ -1359,6 +1624,14 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
     }
     __syncthreads();
     const int nstart = c.ibc[2];
+    if (J.debug_start) {  // dev aid: return a start set instead of the dominant rows
+      for (int t = threadIdx.x; t < r; t += CT) c.best[t] = c.starts[(J.debug_start - 1) * r + t];
+      __syncthreads();
+      if (job.sel_out && c.crank == 0)
+        for (int t = threadIdx.x; t < r; t += CT) job.sel_out[inst * job.sel_stride + t] = c.best[t];
+      cl.sync();
+      return;
+    }
     const long long limit = job.max_iters >= 0 ? job.max_iters : 10LL * m;
     double best_vol = -INFINITY;
     bool have = false;
@@ -1502,9 +1775,23 @@ static bool q_wy_enabled() {
   return on;
 }
 
+// TTP_STARTS=split runs the two starts as separate in-place factorizations.
+static bool fused_starts_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TTP_STARTS");
+    return !(e && strcmp(e, "split") == 0);
+  }();
+  return on;
+}
+
 cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream_t s) {
   ClusterJob job = job_in;
   job.q_wy = q_wy_enabled() ? 1 : 0;
+  job.fused_starts = fused_starts_enabled() ? 1 : 0;
+  {
+    const char* e = getenv("TTP_DEBUG_START");
+    job.debug_start = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+  }
   const int C = job.cl;
   const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr);
   cudaError_t e = ensure_max_smem((const void*)cluster_bond_kernel);
