@@ -213,6 +213,29 @@ int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const double* d_mats, 
                int64_t max_iters, double rank_tol, int64_t* h_sel, int32_t* h_status,
                void* d_ws, size_t ws_bytes, void* stream);
 
+/* K9: Monte Carlo estimate of the discounted min-option payoff
+ * (price_monte_carlo, pricers.py:297-350) for n_inst instances of dimension
+ * d, n_samples paths each.  Parameters per instance (doubles, stride
+ * param_stride >= ttp_mc_param_count(d)):
+ *   [s0 d][drift d][vol d][rates d][sigma d][chol d*d (row-major, lower)]
+ *   [strike][disc][dt]
+ * with drift = (rates - sigma^2/2) T, vol = sigma sqrt(T), disc =
+ * exp(-r (T - t)), dt = T / n_steps (pricers.py:313-330).
+ * scheme 0 = terminal_exact, 1 = euler_path (n_steps Euler steps).
+ * Normals: Philox4x32-10 (Random123) keyed by h_seeds[inst], counter =
+ * (sample lo, sample hi, draw, 0x4D43), two 53-bit uniforms per call and
+ * Box-Muller.  The stream is a function of (seed, sample) only, so results
+ * do not depend on chunking or grid shape; partial sums reduce in a fixed
+ * order.  h_out: n_inst x 2 doubles = (sum, sum of squares) of the
+ * discounted payoffs.                                                      */
+int32_t ttp_mc_param_count(int32_t d);
+size_t ttp_mc_workspace(int32_t n_inst, int64_t n_samples);
+int ttp_mc_price(const double* d_params, int64_t param_stride, int32_t d, int32_t n_inst,
+                 int64_t n_samples, const uint64_t* h_seeds, int32_t scheme, int32_t n_steps,
+                 double* h_out, void* d_ws, size_t ws_bytes, void* stream);
+/* Philox4x32-10 block for known-answer tests: h_ctr[4], h_key[2] -> h_out[4]. */
+int ttp_philox4x32(const uint32_t* h_ctr, const uint32_t* h_key, uint32_t* h_out);
+
 #ifdef __cplusplus
 }
 #endif

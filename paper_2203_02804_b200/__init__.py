@@ -56,5 +56,6 @@ from .pricers import (
     price_fourier_tt_batch,
     table1_hyperparams,
 )
+from .montecarlo import price_monte_carlo, price_monte_carlo_batch
 
 __all__ = [name for name in dir() if not name.startswith("_")]

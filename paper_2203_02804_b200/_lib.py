@@ -157,6 +157,12 @@ SIGNATURES = [
     ("ttp_cross_layout_of", _i32, [_i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(CrossLayout)]),
     ("ttp_cross_workspace", _sz, [ctypes.POINTER(CrossProblem)]),
     ("ttp_cross_run", _i32, [ctypes.POINTER(CrossProblem), ctypes.POINTER(CrossOut), _p, _sz, _p]),
+    ("ttp_mc_param_count", _i32, [_i32]),
+    ("ttp_mc_workspace", _sz, [_i32, _i64]),
+    ("ttp_mc_price", _i32, [_p, _i64, _i32, _i32, _i64, ctypes.POINTER(ctypes.c_uint64), _i32, _i32,
+                            ctypes.POINTER(_f64), _p, _sz, _p]),
+    ("ttp_philox4x32", _i32, [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
+                              ctypes.POINTER(ctypes.c_uint32)]),
     ("ttp_maxvol_workspace", _sz, [_i32, _i64, _i32]),
     ("ttp_maxvol", _i32, [_i32, _i64, _i32, _p, _f64, _i64, _f64, ctypes.POINTER(_i64),
                           ctypes.POINTER(_i32), _p, _sz, _p]),

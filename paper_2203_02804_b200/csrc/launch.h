@@ -20,6 +20,8 @@ enum KernelClass {
   KC_DENSE,
   KC_DENSE_FINAL,
   KC_MISC,
+  KC_MC,
+  KC_MC_FINAL,
   KC_COUNT
 };
 
