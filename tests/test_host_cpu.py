@@ -32,7 +32,7 @@ HEADER = os.path.join(REPO, "include", "ttpricer_b200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|size_t|const char\*)\s+(ttp_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|void|size_t|const char\*)\s+(ttp_\w+)\s*\(",
                                  text, re.M)))
 
 
