@@ -54,6 +54,7 @@ from .pricers import (
     price_fourier_dense_batch,
     price_fourier_tt,
     price_fourier_tt_batch,
+    price_strike_ladder,
     table1_hyperparams,
 )
 from .montecarlo import price_monte_carlo, price_monte_carlo_batch

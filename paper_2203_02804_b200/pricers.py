@@ -279,3 +279,60 @@ def price_fourier_tt(model, grid, cfg_phi, cfg_v, t=0.0, dense_reference="auto",
         raise ValueError(f"model has d={model.d} but grid has d={grid.d}")
     return price_fourier_tt_batch([model], grid, cfg_phi, cfg_v, t=t,
                                   dense_reference=dense_reference, term_cap=term_cap)[0]
+
+
+def price_strike_ladder(model, grid, strikes, cfg_phi, cfg_v, t=0.0, raise_errors=True):
+    """Price one model at a ladder of strikes (the
+    reference's run_strike_sweep, bench.py:478-510, calls price_fourier_tt
+    once per strike).
+
+    phi(-z) does not depend on the strike (pricers.py:234-240), and the
+    reference's per-strike phi crosses all see the same oracle and the same
+    CrossConfig, so they build the same train; here it is built ONCE and
+    reused for every strike, while the strike-dependent payoff crosses run
+    as one batch.  Each price therefore equals the per-strike
+    price_fourier_tt price, at one phi cross instead of len(strikes).
+    """
+    from .market import MarketModel
+    from .tensor_train import DeviceTTBatch
+    if model.d != grid.d:
+        raise ValueError(f"model has d={model.d} but grid has d={grid.d}")
+    strikes = [float(k) for k in strikes]
+    if not strikes:
+        return []
+    _require_admissible(grid)
+    start = time.perf_counter()
+    shape = (grid.points_per_axis,) * grid.d
+    ladder = [MarketModel(r=model.r, sigma=model.sigma, T=model.T, s0=model.s0, strike=k,
+                          corr=model.corr, rates=model.rates, d=model.d) for k in strikes]
+    phi_res, v_res = run_cross_pair(OracleBatch([PhiGridOracle(model, grid)]),
+                                    OracleBatch([PayoffGridOracle(m, grid, conj=True) for m in ladder]),
+                                    shape, cfg_phi, cfg_v)
+    n = len(strikes)
+    err_phi = phi_res.error_for(0)
+    if err_phi is not None:
+        if raise_errors:
+            raise err_phi
+        return [err_phi] * n
+    ph = phi_res.trains
+    kets = DeviceTTBatch(ph.shape, ph.bonds, ph.flat[: ph.stride].repeat(n), n)
+    raw = tt_inner_batch(v_res.trains, kets)
+    wall = time.perf_counter() - start
+    out = []
+    for i, m in enumerate(ladder):
+        err = v_res.error_for(i)
+        if err is not None:
+            if raise_errors:
+                raise err
+            out.append(err)
+            continue
+        value = _prefactor(m, grid, t) * raw[i]
+        out.append(PricingResult(float(value.real), "fourier_tt", wall / n, {
+            "strike": m.strike,
+            "cross_phi": phi_res.reports[0],
+            "cross_v": v_res.reports[i],
+            "imag_part": float(value.imag),
+            "oracle_calls_total": phi_res.reports[0].oracle_calls + v_res.reports[i].oracle_calls,
+            "phi_shared": True,
+        }))
+    return out

@@ -426,3 +426,20 @@ def test_p4_cfg5_single_option_against_reference():
     assert abs(res.price - ref["price"]) <= 1e-3 * abs(ref["price"])
     assert res.diagnostics["cross_phi"].sweeps_used == ref["cross_phi"]["sweeps_used"]
     assert res.diagnostics["cross_v"].sweeps_used == ref["cross_v"]["sweeps_used"]
+
+
+def test_strike_ladder_equals_per_strike_pricing():
+    """one phi train serves the whole ladder; every price
+    equals the per-strike price_fourier_tt price (which is what the
+    reference's run_strike_sweep computes), and tracks the dense sum."""
+    m = P.MarketModel.with_plus_correlation(d=3, beta=0.5, **BENCH)
+    grid = bench_grid(3)
+    cfg = P.CrossConfig(bond_dim=6, seed=1237)
+    strikes = [80.0, 95.0, 100.0, 110.0, 130.0]
+    ladder = P.price_strike_ladder(m, grid, strikes, cfg, cfg)
+    for k, res in zip(strikes, ladder):
+        mk_ = P.MarketModel(r=m.r, sigma=m.sigma, T=m.T, s0=m.s0, strike=k, corr=m.corr, d=3)
+        single = P.price_fourier_tt(mk_, grid, cfg, cfg, dense_reference="auto")
+        assert res.price == single.price
+        assert abs(res.price - single.diagnostics["dense_price"]) <= 1e-3 * abs(single.diagnostics["dense_price"])
+    assert ladder[0].diagnostics["cross_phi"] is ladder[-1].diagnostics["cross_phi"]
