@@ -21,7 +21,7 @@ from .errors import (
     SingularMatrixError,
     StripConditionError,
 )
-from .market import MarketModel, corr_matrix_plus
+from .market import MarketModel, black_scholes_price, corr_matrix_plus
 from .oracles import (
     DeviceOracle,
     OracleBatch,
@@ -58,5 +58,6 @@ from .pricers import (
     table1_hyperparams,
 )
 from .montecarlo import price_monte_carlo, price_monte_carlo_batch
+from .experiments import ExperimentConfig, run_bond_dim_sweep, run_strike_sweep, run_table1
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -90,3 +90,19 @@ class MarketModel:
     def __repr__(self):
         return (f"MarketModel(d={self.d}, r={self.r}, sigma={self.sigma.tolist()}, "
                 f"T={self.T}, s0={self.s0.tolist()}, strike={self.strike})")
+
+
+def black_scholes_price(model, t=0.0):
+    """Closed-form European call for one asset (market.py:173-190):
+    ``S0 Phi(d1) - K e^{-r(T-t)} Phi(d2)`` with scipy's ndtr."""
+    from scipy.special import ndtr
+    if model.d != 1:
+        raise ValueError(f"closed form needs d=1, model has d={model.d}")
+    if t >= model.T:
+        raise ValueError(f"valuation time {t} must precede maturity {model.T}")
+    s0, k, sig = model.s0[0], model.strike, model.sigma[0]
+    tau = model.T - t
+    vol = sig * np.sqrt(tau)
+    d1 = (np.log(s0 / k) + (model.r + 0.5 * sig ** 2) * tau) / vol
+    d2 = d1 - vol
+    return float(s0 * ndtr(d1) - k * np.exp(-model.r * tau) * ndtr(d2))

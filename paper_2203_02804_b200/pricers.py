@@ -281,7 +281,8 @@ def price_fourier_tt(model, grid, cfg_phi, cfg_v, t=0.0, dense_reference="auto",
                                   dense_reference=dense_reference, term_cap=term_cap)[0]
 
 
-def price_strike_ladder(model, grid, strikes, cfg_phi, cfg_v, t=0.0, raise_errors=True):
+def price_strike_ladder(model, grid, strikes, cfg_phi, cfg_v, t=0.0, dense_reference="never",
+                        term_cap=DENSE_TERM_CAP, raise_errors=True):
     """Price one model at a ladder of strikes (the
     reference's run_strike_sweep, bench.py:478-510, calls price_fourier_tt
     once per strike).
@@ -318,6 +319,9 @@ def price_strike_ladder(model, grid, strikes, cfg_phi, cfg_v, t=0.0, raise_error
     kets = DeviceTTBatch(ph.shape, ph.bonds, ph.flat[: ph.stride].repeat(n), n)
     raw = tt_inner_batch(v_res.trains, kets)
     wall = time.perf_counter() - start
+    dense = None
+    if dense_reference == "auto" and grid.n_terms <= term_cap:
+        dense = price_fourier_dense_batch(ladder, grid, t=t, term_cap=term_cap)
     out = []
     for i, m in enumerate(ladder):
         err = v_res.error_for(i)
@@ -327,12 +331,16 @@ def price_strike_ladder(model, grid, strikes, cfg_phi, cfg_v, t=0.0, raise_error
             out.append(err)
             continue
         value = _prefactor(m, grid, t) * raw[i]
-        out.append(PricingResult(float(value.real), "fourier_tt", wall / n, {
+        diag = {
             "strike": m.strike,
             "cross_phi": phi_res.reports[0],
             "cross_v": v_res.reports[i],
             "imag_part": float(value.imag),
             "oracle_calls_total": phi_res.reports[0].oracle_calls + v_res.reports[i].oracle_calls,
             "phi_shared": True,
-        }))
+        }
+        if dense is not None:
+            diag["dense_price"] = dense[i].price
+            diag["eps_trunc"] = float(abs(value.real - dense[i].price) / abs(dense[i].price))
+        out.append(PricingResult(float(value.real), "fourier_tt", wall / n, diag))
     return out
