@@ -209,7 +209,7 @@ __device__ __forceinline__ cplx col_dotc(const CC& c, int ci, int cj, int l0, in
   const cplx* b = c.Ws + (long long)cj * c.ldw;
   cplx acc = mk(0.0, 0.0);
   int l = l0;
-  constexpr int RB = 4;
+  constexpr int RB = 8;
   for (; l + 32 * (RB - 1) < nl; l += 32 * RB) {
     cplx x[RB], y[RB];
 #pragma unroll
