@@ -47,7 +47,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--batch", type=int, default=148, help="options per GPU per step")
+    ap.add_argument("--batch", type=int, default=592,
+                    help="options per GPU per step (4 x 148: throughput saturates here, profiles/r01/batch_sweep.json)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="options in the CPU baseline sample (0 = one per core)")
