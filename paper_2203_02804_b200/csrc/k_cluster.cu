@@ -66,6 +66,7 @@ namespace {
 constexpr int CT = CLUSTER_THREADS;
 constexpr int CW = CT / 32;
 constexpr int RMAX = 64;
+constexpr int QX_ROWS = 64;  // rows per staged tile of the DMMA Q*X products
 
 struct __align__(16) Rec {
   double v;
@@ -130,6 +131,7 @@ struct CC {
   WCand* wrec2;    // [2][CW] second candidate stream (fused starts)
   int* rpos2;      // ldw: LU positions (fused starts)
   cplx* sp;        // 8r scratch vectors (fused starts)
+  double* qtile;   // QX_ROWS x (2r padded + 4) interleaved Q rows (DMMA Q*X), or nullptr
   cplx* wrow;      // [2][CW][r] per-warp candidate row data
   cplx* bvec;      // [CW][2r] per-warp private broadcast vectors
   Cand* wcand;     // CW
@@ -255,6 +257,8 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
   t.wrec2 = (WCand*)take(sizeof(WCand) * 2 * CW);
   t.rpos2 = (int*)take(sizeof(int) * ldw);
   t.sp = (cplx*)take(sizeof(cplx) * 8 * r);
+  // staged Q row tile of the DMMA Q*X products (global-slice mode, r <= 32)
+  t.qtile = (global_slice && r <= 32) ? (double*)take(sizeof(double) * QX_ROWS * (((2 * r + 3) & ~3) + 4)) : nullptr;
   t.wrow = (cplx*)take(sizeof(cplx) * 2 * CW * r);
   t.bvec = (cplx*)take(sizeof(cplx) * CW * 2 * r);
   t.wcand = (Cand*)take(sizeof(Cand) * CW);
@@ -268,7 +272,7 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
     c->flags = t.flags; c->first = t.first; c->sel = t.sel; c->best = t.best; c->starts = t.starts;
     c->vn1 = t.vn1; c->vn2 = t.vn2; c->rpos = t.rpos; c->rec = t.rec; c->wcand = t.wcand;
     c->wrec = t.wrec; c->wrow = t.wrow; c->bvec = t.bvec;
-    c->wrec2 = t.wrec2; c->rpos2 = t.rpos2; c->sp = t.sp;
+    c->wrec2 = t.wrec2; c->rpos2 = t.rpos2; c->sp = t.sp; c->qtile = t.qtile;
     c->wss = t.wss; c->ibc = t.ibc; c->dbc = t.dbc; c->cbc = t.cbc;
   }
   return off;
@@ -856,6 +860,70 @@ __device__ double invert_rows(const CC& c, const int* rows) {
   return gauss_jordan_fast<CT>(c.aug, r, c.vec2, c.ibc);
 }
 
+// My rows of Q X on the FP64 tensor cores (DMMA m8n8k4), r <= 32: Q rows
+// are staged QX_ROWS at a time as interleaved reals (the A operand as
+// stored); X (complex r x r, ld ldx) is expanded once per call into the
+// B-fragment registers of each warp (warp w owns real n-tile w & 7 and
+// m-tiles (w >> 3) + 2i of every staged tile).  sink(l, j, value) receives
+// every output entry.  Same products as rowblock_X up to the association of
+// the r-term sums.
+template <class Sink>
+__device__ void qx_dmma(const CC& c, const cplx* X, int ldx, Sink sink) {
+  const int r = c.r, lo = c.row0, nl = c.nrows, m = c.m;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int Kp = (2 * r + 3) & ~3, ldA = Kp + 4, nks = Kp / 4;
+  const int ntn = (2 * r + 7) / 8;
+  const int nt = warp & 7, mgrp = warp >> 3;
+  constexpr int MG = CW / 8;  // warp groups over m-tiles
+  const bool active = nt < ntn;
+  double breg[16];
+#pragma unroll
+  for (int ks = 0; ks < 16; ++ks) {
+    const int k = 4 * ks + tig, n = nt * 8 + gid;
+    const int a = k >> 1, col = n >> 1;
+    double b = 0.0;
+    if (ks < nks && a < r && col < r) {
+      const cplx x = X[a * ldx + col];
+      b = ((k & 1) == (n & 1)) ? x.x : ((n & 1) ? x.y : -x.y);
+    }
+    breg[ks] = b;
+  }
+  double* tile = c.qtile;
+  for (int e = threadIdx.x; e < QX_ROWS * (Kp - 2 * r); e += CT) {
+    const int row = e / (Kp - 2 * r), k = 2 * r + (e - row * (Kp - 2 * r));
+    tile[row * ldA + k] = 0.0;
+  }
+  for (int l0 = 0; l0 < nl; l0 += QX_ROWS) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < QX_ROWS * r; e += CT) {
+      const int t = e / QX_ROWS, row = e - t * QX_ROWS;
+      const int l = l0 + row;
+      const cplx v = (l < nl) ? c.Qg[(long long)t * m + lo + l] : mk(0.0, 0.0);
+      tile[row * ldA + 2 * t] = v.x;
+      tile[row * ldA + 2 * t + 1] = v.y;
+    }
+    __syncthreads();
+    if (active) {
+      for (int mi = mgrp; mi < QX_ROWS / 8; mi += MG) {
+        const int m0 = mi * 8;
+        double c0 = 0.0, c1 = 0.0;
+        const double* arow = tile + (m0 + gid) * ldA + tig;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          if (ks < nks) {
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(c0), "+d"(c1) : "d"(arow[4 * ks]), "d"(breg[ks]));
+          }
+        }
+        const int l = l0 + m0 + gid, j = nt * 4 + tig;
+        if (l < nl && j < r) sink(l, j, mk(c0, c1));
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // B = Q X for my rows (into Ws) and for the selected rows (selb); returns my
 // best |B| candidate (key = global row-major index).
 __device__ Cand form_B(const CC& c) {
@@ -863,6 +931,13 @@ __device__ Cand form_B(const CC& c) {
   const cplx* X = c.aug + r;
   Cand a{-1.0, LLONG_MAX, -1};
   constexpr int JB = 16;
+  if (c.qtile) {
+    qx_dmma(c, X, ld, [&](int l, int j, cplx v) {
+      Wl(c, l, j) = v;
+      const Cand b{cabs2(v), (long long)(lo + l) * r + j, l};
+      if (cand_better(b, a)) a = b;
+    });
+  } else
   for (int l = threadIdx.x; l < nl; l += CT) {
     const cplx* q = Qrow(c, lo + l);
     for (int j0 = 0; j0 < r; j0 += JB) {
@@ -1710,6 +1785,14 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
   }
   cplx* core = job.core_out + inst * job.core_stride;
   const cplx* X = c.aug + r;
+  if (c.qtile) {
+    const int wm = job.write_mode;
+    qx_dmma(c, X, 2 * r, [&](int l, int j, cplx v) {
+      const int g = c.row0 + l;
+      if (wm == 1) core[(long long)g * r + j] = v;
+      else core[(long long)j * m + g] = v;
+    });
+  } else
   for (int l = threadIdx.x; l < c.nrows; l += CT) {
     const int g = c.row0 + l;
     const cplx* q = Qrow(c, g);
