@@ -42,8 +42,8 @@ TTDev tt_dev(const ttp_tt_batch& b) {
   return t;
 }
 
-constexpr int INNER_THREADS = 256;
-constexpr int INNER_ACC = 16;  // (64*64)/256 accumulators per thread max
+constexpr int INNER_THREADS = 512;
+constexpr int INNER_ACC = 8;  // (64*64)/512 accumulators per thread max
 
 __global__ void __launch_bounds__(INNER_THREADS)
 tt_inner_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) {
