@@ -229,6 +229,25 @@ def _status_error(status, bond):
     return RuntimeError(f"cross failed with status {status}")
 
 
+def cross_bytes_per_instance(shape, cfg):
+    """Device bytes one instance of tt_cross_batch needs (workspace + cores +
+    index sets), from the library's own workspace rule (ttp_cross_workspace)."""
+    lib = _lib.load_library()
+    shape = tuple(int(n) for n in shape)
+    d = len(shape)
+    lay = _Layout(shape, min(cfg.bond_dim, MAX_BOND))
+
+    def ws(n):
+        prob = _lib.CrossProblem(
+            d=d, n_inst=n, h_shape=lay.shape.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            cfg=_lib.CrossCfg(bond_dim=cfg.bond_dim if d > 1 else 1, max_sweeps=cfg.max_sweeps,
+                              eps_tol=cfg.eps_tol, n_conv_samples=cfg.n_conv_samples,
+                              maxvol_slack=cfg.maxvol_slack, oracle_call_budget=-1))
+        return lib.ttp_cross_workspace(ctypes.byref(prob))
+
+    return (ws(2) - ws(1)) + 16 * lay.core_stride + 8 * lay.set_stride
+
+
 def tt_cross_batch(oracles, shape, cfg, with_reports=True):
     """Batched TT-cross of independent oracles sharing ``shape`` and ``cfg``.
 

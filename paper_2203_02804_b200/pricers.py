@@ -227,6 +227,16 @@ def run_cross_pair(phi_batch, v_batch, shape, cfg_phi, cfg_v, with_reports=True)
     return out["phi"], out["v"]
 
 
+def max_batch(shape, cfg_phi, cfg_v, fraction=0.6):
+    """Largest number of instances whose phi and vhat crosses fit together in
+    `fraction` of the device memory currently free."""
+    from .cross import cross_bytes_per_instance
+    torch = _lib.require_device()
+    free, _ = torch.cuda.mem_get_info()
+    per = cross_bytes_per_instance(shape, cfg_phi) + cross_bytes_per_instance(shape, cfg_v)
+    return max(1, int(fraction * free) // max(1, per))
+
+
 def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference="never",
                            term_cap=DENSE_TERM_CAP, raise_errors=True):
     """Price many independent options on one grid with the device TT path.
@@ -240,8 +250,18 @@ def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference=
         if m.d != grid.d:
             raise ValueError(f"model has d={m.d} but grid has d={grid.d}")
     _require_admissible(grid)
-    start = time.perf_counter()
     shape = (grid.points_per_axis,) * grid.d
+    # memory-aware batching: instances that do not fit one launch pair run in
+    # consecutive chunks (results identical: instances are independent)
+    chunk = max_batch(shape, cfg_phi, cfg_v)
+    if len(models) > chunk:
+        out = []
+        for i0 in range(0, len(models), chunk):
+            out.extend(price_fourier_tt_batch(models[i0:i0 + chunk], grid, cfg_phi, cfg_v, t=t,
+                                              dense_reference=dense_reference, term_cap=term_cap,
+                                              raise_errors=raise_errors))
+        return out
+    start = time.perf_counter()
     phi_res, v_res = run_cross_pair(OracleBatch([PhiGridOracle(m, grid) for m in models]),
                                     OracleBatch([PayoffGridOracle(m, grid, conj=True) for m in models]),
                                     shape, cfg_phi, cfg_v)
