@@ -84,8 +84,8 @@ CrossWs carve_cross(const ttp_cross_layout& L, int n_inst, long long M, unsigned
   const long long mr = (L.max_rows + 16) * (long long)L.max_rank;
   w.mat_stride = mr;
   w.v_stride = M * (long long)L.max_rank;
-  w.iw_stride = 2 * L.max_rows;
-  w.dw_stride = 2 * L.max_rows;
+  w.iw_stride = 2 * (L.max_rows + 16);  // also the per-CTA row arrays of big cluster jobs
+  w.dw_stride = 2 * (L.max_rows + 16);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     unsigned char* p = base ? base + off : nullptr;
@@ -248,11 +248,16 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
   // shared-memory clusters (more instances in flight per barrier round);
   // smaller blocks run fastest on the one-CTA kernel.
   const long long block_bytes = (long long)bj.m * bj.r * (long long)sizeof(cplx);
-  const bool auto_l2 = bond_path_mode() == 0 && block_bytes >= (1LL << 20) && n > 16;
+  // small batches of blocks too large for a shared-memory cluster (r = 64,
+  // cfg5) also take the global-slice kernel, with more CTAs per instance
+  const bool smem_fits = !force_v0() && pick_cluster_size(bj.m, bj.r, smem_optin_limit()) > 0;
+  const bool auto_l2 = bond_path_mode() == 0 && block_bytes >= (1LL << 20) && (n > 16 || !smem_fits);
   if (bond_path_mode() == 3 || auto_l2) {
     ClusterJob cj{};
     cj.b = bj;
-    const int want = bond_path_mode() == 3 ? l2_cluster_size() : 2;
+    int small_c = 2;
+    while (small_c < 16 && n * small_c * 2 <= 148) small_c *= 2;
+    const int want = bond_path_mode() == 3 ? l2_cluster_size() : (n > 16 ? 2 : small_c);
     cj.cl = std::min(want, std::max(1, bj.m / std::max(1, bj.r)));
     cj.src_mode = 0;
     cj.fiber_fast = fiber_fast_enabled() ? 1 : 0;
@@ -261,6 +266,7 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
     cj.Qg = w.A;
     cj.q_stride = w.mat_stride;
     cj.Wg = w.W;
+    cj.Sg = w.B;
     cj.wg_stride = w.mat_stride;
     if (max_active_clusters(cj) > 0) {
       TTP_CUDA_CHECK(launch_cluster_bond(cj, n, s));

@@ -56,6 +56,8 @@ struct ClusterJob {
   int fiber_fast;         // src_mode 0: separable evaluation allowed (fiber_fast.cuh)
   int q_wy;               // form Q in compact-WY form (else zung2r rounds)
   int fused_starts;       // both dominant-row starts in one read-only pass sequence
+  int big;                // per-row arrays and B[sel,:] in global memory (set by the launcher)
+  cplx* Sg;               // global-slice mode: B buffer (holds B[sel,:] in big mode), stride wg_stride
   int debug_start;        // dev aid (TTP_DEBUG_START=1|2): return start set 1 or 2
   OracleDev oracle;
   FiberJob fiber;         // index-set views and geometry (out/ld unused)
@@ -71,7 +73,7 @@ struct ClusterJob {
   long long wg_stride;
 };
 
-size_t cluster_smem_bytes(int m, int r, int C, bool global_slice = false);
+size_t cluster_smem_bytes(int m, int r, int C, bool global_slice = false, bool big = false);
 int pick_cluster_size(int m, int r, size_t smem_limit);  // 0 if no cluster fits
 int max_active_clusters(const ClusterJob& job);
 cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s);

@@ -133,7 +133,6 @@ struct CC {
   cplx* sp;        // 8r scratch vectors (fused starts)
   double* qtile;   // QX_ROWS x (2r padded + 4) interleaved Q rows (DMMA Q*X), or nullptr
   cplx* wrow;      // [2][CW][r] per-warp candidate row data
-  cplx* bvec;      // [CW][2r] per-warp private broadcast vectors
   Cand* wcand;     // CW
   Ssq* wss;        // CW
   int* ibc;        // 8
@@ -226,7 +225,11 @@ __device__ __forceinline__ cplx col_dotc(const CC& c, int ci, int cj, int l0, in
   return acc;
 }
 
-__host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, bool global_slice = false) {
+// big: (global-slice mode, blocks whose normal carve exceeds shared memory,
+// e.g. r = 64) the per-row arrays vn1/vn2/rpos/rpos2 and B[sel,:] live in
+// global memory (the instance's dwork/iwork and B buffers) instead.
+__host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, bool global_slice = false,
+                                 bool big = false) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     unsigned char* p = base ? base + off : nullptr;
@@ -236,7 +239,7 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
   CC t;
   t.Ws = global_slice ? nullptr : (cplx*)take(sizeof(cplx) * (size_t)ldw * r);
   t.aug = (cplx*)take(sizeof(cplx) * 2 * r * r);
-  t.selb = (cplx*)take(sizeof(cplx) * r * r);
+  t.selb = big ? nullptr : (cplx*)take(sizeof(cplx) * r * r);
   t.vec = (cplx*)take(sizeof(cplx) * r);
   t.vec2 = (cplx*)take(sizeof(cplx) * 5 * r);  // also Gauss-Jordan scratch
   t.tau = (cplx*)take(sizeof(cplx) * r);
@@ -249,18 +252,17 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
   t.sel = (int*)take(sizeof(int) * r);
   t.best = (int*)take(sizeof(int) * r);
   t.starts = (int*)take(sizeof(int) * 2 * r);
-  t.vn1 = (double*)take(sizeof(double) * ldw);
-  t.vn2 = (double*)take(sizeof(double) * ldw);
-  t.rpos = (int*)take(sizeof(int) * ldw);
+  t.vn1 = big ? nullptr : (double*)take(sizeof(double) * ldw);
+  t.vn2 = big ? nullptr : (double*)take(sizeof(double) * ldw);
+  t.rpos = big ? nullptr : (int*)take(sizeof(int) * ldw);
   t.rec = (Rec*)take(sizeof(Rec) * 2);
   t.wrec = (WCand*)take(sizeof(WCand) * 2 * CW);
   t.wrec2 = (WCand*)take(sizeof(WCand) * 2 * CW);
-  t.rpos2 = (int*)take(sizeof(int) * ldw);
+  t.rpos2 = big ? nullptr : (int*)take(sizeof(int) * ldw);
   t.sp = (cplx*)take(sizeof(cplx) * 8 * r);
   // staged Q row tile of the DMMA Q*X products (global-slice mode, r <= 32)
   t.qtile = (global_slice && r <= 32) ? (double*)take(sizeof(double) * QX_ROWS * (((2 * r + 3) & ~3) + 4)) : nullptr;
   t.wrow = (cplx*)take(sizeof(cplx) * 2 * CW * r);
-  t.bvec = (cplx*)take(sizeof(cplx) * CW * 2 * r);
   t.wcand = (Cand*)take(sizeof(Cand) * CW);
   t.wss = (Ssq*)take(sizeof(Ssq) * CW);
   t.ibc = (int*)take(sizeof(int) * 16);
@@ -271,7 +273,7 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
     c->tau = t.tau; c->betas = t.betas; c->cn1 = t.cn1; c->cn2 = t.cn2; c->colmap = t.colmap;
     c->flags = t.flags; c->first = t.first; c->sel = t.sel; c->best = t.best; c->starts = t.starts;
     c->vn1 = t.vn1; c->vn2 = t.vn2; c->rpos = t.rpos; c->rec = t.rec; c->wcand = t.wcand;
-    c->wrec = t.wrec; c->wrow = t.wrow; c->bvec = t.bvec;
+    c->wrec = t.wrec; c->wrow = t.wrow;
     c->wrec2 = t.wrec2; c->rpos2 = t.rpos2; c->sp = t.sp; c->qtile = t.qtile;
     c->wss = t.wss; c->ibc = t.ibc; c->dbc = t.dbc; c->cbc = t.cbc;
   }
@@ -972,7 +974,7 @@ __device__ Cand form_B(const CC& c) {
 // that row's data; after the cluster barrier every warp independently finds
 // the cluster-wide winner among the C*CW records and loads the winning row,
 // so a step needs exactly one barrier (the cluster barrier) and no block
-// barrier.  Per-warp copies of the broadcast vectors live in c.bvec.
+// barrier.
 // ======================================================================
 __device__ __forceinline__ void warp_publish(const CC& c, int par, const Cand& a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1662,8 +1664,15 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
   c.nrows = max(0, min(job.m, c.row0 + ms) - c.row0);
   c.ldw = ms;
   c.Qg = J.Qg + inst * J.q_stride;
-  carve(smem_raw, ms, job.r, &c, J.Wg != nullptr);
+  carve(smem_raw, ms, job.r, &c, J.Wg != nullptr, J.big != 0);
   if (J.Wg) c.Ws = J.Wg + inst * J.wg_stride + (long long)c.crank * ms * job.r;
+  if (J.big) {
+    c.vn1 = job.dwork + inst * job.dw_stride + (long long)c.crank * 2 * ms;
+    c.vn2 = c.vn1 + ms;
+    c.rpos = job.iwork + inst * job.iw_stride + (long long)c.crank * 2 * ms;
+    c.rpos2 = c.rpos + ms;
+    c.selb = J.Sg + inst * J.wg_stride + (long long)c.crank * job.r * job.r;
+  }
   int par = 0;
   const int r = c.r, m = c.m;
 
@@ -1834,9 +1843,30 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
 
 int max_active_clusters_query(int C, size_t smem);
 
-size_t cluster_smem_bytes(int m, int r, int C, bool global_slice) {
+size_t cluster_smem_bytes(int m, int r, int C, bool global_slice, bool big) {
   const int ms = (m + C - 1) / C;
-  return carve(nullptr, ms, r, nullptr, global_slice);
+  return carve(nullptr, ms, r, nullptr, global_slice, big);
+}
+
+static size_t cluster_smem_limit() {
+  static const size_t lim = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, (const void*)cluster_bond_kernel);
+    return (size_t)v - fa.sharedSizeBytes;
+  }();
+  return lim;
+}
+
+// global-slice jobs whose normal carve does not fit shared memory switch to
+// the big layout (needs the instance's dwork/iwork and the B buffer)
+static void resolve_big(ClusterJob& job) {
+  job.big = 0;
+  if (job.Wg && job.Sg && job.b.dwork && job.b.iwork &&
+      cluster_smem_bytes(job.b.m, job.b.r, job.cl, true, false) > cluster_smem_limit())
+    job.big = 1;
 }
 
 int pick_cluster_size(int m, int r, size_t smem_limit) {
@@ -1869,6 +1899,7 @@ static bool fused_starts_enabled() {
 
 cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream_t s) {
   ClusterJob job = job_in;
+  resolve_big(job);
   job.q_wy = q_wy_enabled() ? 1 : 0;
   job.fused_starts = fused_starts_enabled() ? 1 : 0;
   {
@@ -1876,7 +1907,7 @@ cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream
     job.debug_start = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
   }
   const int C = job.cl;
-  const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr);
+  const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr, job.big != 0);
   cudaError_t e = ensure_max_smem((const void*)cluster_bond_kernel);
   if (e != cudaSuccess) return e;
   if (C > 8) {
@@ -1903,9 +1934,12 @@ cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream
   return cudaGetLastError();
 }
 
-int max_active_clusters(const ClusterJob& job) {
+int max_active_clusters(const ClusterJob& job_in) {
+  ClusterJob job = job_in;
+  resolve_big(job);
   const int C = job.cl;
-  const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr);
+  const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr, job.big != 0);
+  if (smem > cluster_smem_limit()) return 0;
   static std::mutex mu;
   static std::map<std::pair<int, size_t>, int> cache;
   {
