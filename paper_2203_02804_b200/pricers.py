@@ -227,13 +227,26 @@ def run_cross_pair(phi_batch, v_batch, shape, cfg_phi, cfg_v, with_reports=True)
     return out["phi"], out["v"]
 
 
-def max_batch(shape, cfg_phi, cfg_v, fraction=0.6):
+_PER_INSTANCE = {}
+_DEVICE_TOTAL = []
+
+
+def max_batch(shape, cfg_phi, cfg_v, n=None, fraction=0.6):
     """Largest number of instances whose phi and vhat crosses fit together in
-    `fraction` of the device memory currently free."""
+    `fraction` of the device memory currently free.  Batches of n instances
+    that need under a third of the device's total memory skip the (slow)
+    free-memory query and are returned as they are."""
     from .cross import cross_bytes_per_instance
     torch = _lib.require_device()
+    key = (tuple(shape), cfg_phi.bond_dim, cfg_phi.n_conv_samples, cfg_v.bond_dim, cfg_v.n_conv_samples)
+    if key not in _PER_INSTANCE:
+        _PER_INSTANCE[key] = cross_bytes_per_instance(shape, cfg_phi) + cross_bytes_per_instance(shape, cfg_v)
+    per = _PER_INSTANCE[key]
+    if not _DEVICE_TOTAL:
+        _DEVICE_TOTAL.append(torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory)
+    if n is not None and n * per <= _DEVICE_TOTAL[0] // 3:
+        return n
     free, _ = torch.cuda.mem_get_info()
-    per = cross_bytes_per_instance(shape, cfg_phi) + cross_bytes_per_instance(shape, cfg_v)
     return max(1, int(fraction * free) // max(1, per))
 
 
@@ -253,7 +266,7 @@ def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference=
     shape = (grid.points_per_axis,) * grid.d
     # memory-aware batching: instances that do not fit one launch pair run in
     # consecutive chunks (results identical: instances are independent)
-    chunk = max_batch(shape, cfg_phi, cfg_v)
+    chunk = max_batch(shape, cfg_phi, cfg_v, n=len(models))
     if len(models) > chunk:
         out = []
         for i0 in range(0, len(models), chunk):
