@@ -443,3 +443,34 @@ def test_strike_ladder_equals_per_strike_pricing():
         assert res.price == single.price
         assert abs(res.price - single.diagnostics["dense_price"]) <= 1e-3 * abs(single.diagnostics["dense_price"])
     assert ladder[0].diagnostics["cross_phi"] is ladder[-1].diagnostics["cross_phi"]
+
+
+def test_memory_aware_chunks_equal_one_launch(monkeypatch):
+    """price_fourier_tt_batch splits batches that do not fit device memory
+    (cfg3's 4096 instances); instances are independent, so chunked prices
+    equal the one-launch prices bitwise."""
+    from paper_2203_02804_b200 import pricers
+    spec = configs.CONFIGS[3]
+    models = [configs.make_model(3, i) for i in range(12)]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    whole = [r.price for r in P.price_fourier_tt_batch(models, spec.grid, cfg, cfg)]
+    monkeypatch.setattr(pricers, "max_batch", lambda *a, **k: 5)
+    chunked = [r.price for r in P.price_fourier_tt_batch(models, spec.grid, cfg, cfg)]
+    assert chunked == whole
+
+
+def test_cfg5_big_layout_batch_equals_single():
+    """r = 64 blocks run the global-slice cluster kernel in its big layout;
+    a batch of two equals two single-option runs bitwise."""
+    spec = configs.CONFIGS[5]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed, max_sweeps=1)
+    models = [configs.make_model(5, i) for i in range(2)]
+    shape = (spec.grid.points_per_axis,) * spec.d
+    batch = P.tt_cross_batch(P.OracleBatch([P.PhiGridOracle(m, spec.grid) for m in models]), shape, cfg)
+    for i, m in enumerate(models):
+        one = P.tt_cross_batch(P.OracleBatch([P.PhiGridOracle(m, spec.grid)]), shape, cfg)
+        assert one.reports[0].to_dict() == batch.reports[i].to_dict()
+        a = one.trains.to_trains()[0]
+        b = batch.trains.to_trains()[i]
+        for ca, cb in zip(a.cores, b.cores):
+            np.testing.assert_array_equal(ca, cb)
