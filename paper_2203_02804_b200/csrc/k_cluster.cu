@@ -1515,11 +1515,14 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
   invert_rows(c, c.sel);
   Cand a = form_B(c);
   int status = TTP_ERR_MAXVOL_ITER;
+  SP_BEGIN(spt);
   for (long long it = 0;; ++it) {
     a = warp_cand(a);
     __syncwarp();
     warp_publish(c, par, a);
+    SP(spt, 8);
     cl.sync();
+    SP(spt, 9);
     if (warp == 0) {
       const Winner W = warp_winner(cl, c, par);
       const int i = W.w.row;
@@ -1545,8 +1548,10 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
         c.ibc[5] = j;
         c.ibc[6] = done;
       }
+      SP(spt, 10);
     }
     __syncthreads();
+    SP(spt, 11);
     const int i = c.ibc[4], j = c.ibc[5], done = c.ibc[6];
     if (it >= limit) break;  // guard exhausted (cross.py:127-139)
     if (done) {
@@ -1567,6 +1572,7 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
       if (lane + 32 < r) c.selb[q * r + lane + 32] = y1;
     }
     if (threadIdx.x == 0) c.sel[j] = i;
+    SP(spt, 12);
     a = Cand{-1.0, LLONG_MAX, -1};
     for (int l = threadIdx.x; l < nl; l += CT) {
       const cplx blj = Wl(c, l, j);
@@ -1592,6 +1598,7 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
         if (cand_better(b, a)) a = b;
       }
     }
+    SP(spt, 13);
     if ((it + 1) % 64 == 0) {
       __syncthreads();
       invert_rows(c, c.sel);

@@ -42,6 +42,6 @@ for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
     sub = ["pivot+recomp", "partials", "clsync", "reduce", "update", "-", "zung2r"]
     print("    colbasis sub-phases (all bonds of the sweep): " + " ".join(
         f"{sub[k]}={out[16 + k] / ghz / 1e3:.1f}us" for k in range(7)), flush=True)
-    sub2 = ["s1.local", "s1.publish", "s1.clsync", "s1.winner", "s1.reflector", "s1.barrier"]
-    print("    start1 sub-phases (all bonds): " + " ".join(
+    sub2 = ["sw.publish", "sw.clsync", "sw.winner", "sw.barrier", "sw.selb", "sw.rowpass"]
+    print("    swap sub-phases (all bonds, both runs): " + " ".join(
         f"{sub2[k]}={out[24 + k] / ghz / 1e3:.1f}us" for k in range(6)), flush=True)
