@@ -366,6 +366,18 @@ def main():
     roofline = kernel_roofline(dom_name)
     roofline["note"] = ("durations from one untimed, stream-serialized step (the timed region overlaps the "
                         "phi and vhat crosses on two streams); algorithmic flops per SURVEY.md 8(d)")
+    # the bond kernel is memory bound: its measured DRAM traffic (ncu, same
+    # batch) per event-timed launch, against the measured HBM copy peak
+    try:
+        hbm_peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except (OSError, ValueError):
+        hbm_peak = None
+    if traffic and roofline.get("avg_launch_ms") and hbm_peak:
+        rate = traffic / (roofline["avg_launch_ms"] / 1e3) / 1e9
+        roofline["dram"] = {"bytes_per_launch": traffic, "achieved_gbs": rate, "peak_gbs": hbm_peak,
+                            "frac": rate / hbm_peak,
+                            "source": "profiles/ncu_traffic.json (dram__bytes_read+write, ncu --set full, "
+                                      "same batch) / avg_launch_ms; MEASURED_PEAKS.json hbm_gbs"}
     secondary = [kernel_roofline(k) for k in ("conv_site_kernel", "tt_inner_kernel") if k != dom_name]
 
     cpu_baseline = None
