@@ -197,6 +197,12 @@ size_t ttp_dense_workspace(int32_t n_inst, int64_t n_terms);
 int ttp_dense_sum(const ttp_oracle* phi, const ttp_oracle* vhat, const int32_t* h_shape,
                   const int32_t* d_shape, int32_t n_inst, double* h_out, void* d_ws,
                   size_t ws_bytes, void* stream);
+/* Same sum over the flat C-order term range [first, first + count) (count < 0:
+ * to the end) -- the per-rank share of a dense cross-check sharded by flat
+ * index range across GPUs; partials combine in rank order. */
+int ttp_dense_sum_range(const ttp_oracle* phi, const ttp_oracle* vhat, const int32_t* h_shape,
+                        const int32_t* d_shape, int32_t n_inst, int64_t first, int64_t count,
+                        double* h_out, void* d_ws, size_t ws_bytes, void* stream);
 
 /* K3-K6 batched TT-cross (cross.py:358-453). */
 int ttp_cross_layout_of(int32_t d, const int32_t* h_shape, int32_t bond_dim,

@@ -154,6 +154,8 @@ SIGNATURES = [
     ("ttp_dense_workspace", _sz, [_i32, _i64]),
     ("ttp_dense_sum", _i32, [ctypes.POINTER(Oracle), ctypes.POINTER(Oracle), ctypes.POINTER(_i32),
                              _p, _i32, ctypes.POINTER(_f64), _p, _sz, _p]),
+    ("ttp_dense_sum_range", _i32, [ctypes.POINTER(Oracle), ctypes.POINTER(Oracle), ctypes.POINTER(_i32),
+                                   _p, _i32, _i64, _i64, ctypes.POINTER(_f64), _p, _sz, _p]),
     ("ttp_cross_layout_of", _i32, [_i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(CrossLayout)]),
     ("ttp_cross_workspace", _sz, [ctypes.POINTER(CrossProblem)]),
     ("ttp_cross_run", _i32, [ctypes.POINTER(CrossProblem), ctypes.POINTER(CrossOut), _p, _sz, _p]),

@@ -16,12 +16,13 @@ constexpr int DENSE_THREADS = 256;
 constexpr int DENSE_SLABS = 1184;  // 8 CTAs per SM on 148 SMs
 
 __global__ void __launch_bounds__(DENSE_THREADS)
-dense_partial_kernel(OracleDev phi, OracleDev vhat, long long n_terms, cplx* __restrict__ part) {
+dense_partial_kernel(OracleDev phi, OracleDev vhat, long long first, long long count,
+                     cplx* __restrict__ part) {
   const int inst = blockIdx.y;
   const int slab = blockIdx.x;
-  const long long per = (n_terms + gridDim.x - 1) / gridDim.x;
-  const long long lo = slab * per;
-  const long long hi = min(n_terms, lo + per);
+  const long long per = (count + gridDim.x - 1) / gridDim.x;
+  const long long lo = first + slab * per;
+  const long long hi = min(first + count, lo + per);
   const int d = phi.d;
   cplx acc = mk(0.0, 0.0);
   int idx[TTP_MAX_D];
@@ -76,9 +77,19 @@ extern "C" size_t ttp_dense_workspace(int32_t n_inst, int64_t) {
   return sizeof(cplx) * ((size_t)n_inst * DENSE_SLABS + (size_t)n_inst);
 }
 
+extern "C" int ttp_dense_sum_range(const ttp_oracle* phi, const ttp_oracle* vhat, const int32_t* h_shape,
+                                   const int32_t* d_shape, int32_t n_inst, int64_t first, int64_t count,
+                                   double* h_out, void* d_ws, size_t ws_bytes, void* stream);
+
 extern "C" int ttp_dense_sum(const ttp_oracle* phi, const ttp_oracle* vhat, const int32_t* h_shape,
                              const int32_t* d_shape, int32_t n_inst, double* h_out, void* d_ws,
                              size_t ws_bytes, void* stream) {
+  return ttp_dense_sum_range(phi, vhat, h_shape, d_shape, n_inst, 0, -1, h_out, d_ws, ws_bytes, stream);
+}
+
+extern "C" int ttp_dense_sum_range(const ttp_oracle* phi, const ttp_oracle* vhat, const int32_t* h_shape,
+                                   const int32_t* d_shape, int32_t n_inst, int64_t first, int64_t count,
+                                   double* h_out, void* d_ws, size_t ws_bytes, void* stream) {
   if (!phi || !vhat || phi->kind != TTP_ORACLE_PHI_GBM || vhat->kind != TTP_ORACLE_VHAT_MIN ||
       phi->d != vhat->d || phi->d < 1 || phi->d > TTP_MAX_D || n_inst < 0)
     return ttp_fail(TTP_ERR_INVALID, "dense_sum: expects a PHI_GBM and a VHAT_MIN oracle");
@@ -88,6 +99,9 @@ extern "C" int ttp_dense_sum(const ttp_oracle* phi, const ttp_oracle* vhat, cons
     if (n_terms > (1LL << 62) / h_shape[k]) return ttp_fail(TTP_ERR_CAPACITY, "dense_sum: grid too large");
     n_terms *= h_shape[k];
   }
+  if (count < 0) count = n_terms - first;
+  if (first < 0 || first > n_terms || count > n_terms - first)
+    return ttp_fail(TTP_ERR_INVALID, "dense_sum: term range outside the grid");
   if (ws_bytes < ttp_dense_workspace(n_inst, n_terms))
     return ttp_fail(TTP_ERR_WORKSPACE, "dense_sum: workspace too small");
   if (n_inst == 0) return TTP_OK;
@@ -99,7 +113,7 @@ extern "C" int ttp_dense_sum(const ttp_oracle* phi, const ttp_oracle* vhat, cons
   dim3 grid(DENSE_SLABS, (unsigned)n_inst);
   {
     LaunchScope _ls(KC_DENSE, s);
-    dense_partial_kernel<<<grid, DENSE_THREADS, 0, s>>>(a, b, n_terms, part);
+    dense_partial_kernel<<<grid, DENSE_THREADS, 0, s>>>(a, b, first, count, part);
   }
   TTP_CUDA_CHECK(cudaGetLastError());
   {

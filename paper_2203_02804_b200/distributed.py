@@ -63,3 +63,39 @@ def gather_records(local, n_total, device=None):
         rows.append(parts[r].cpu().numpy()[: hi - lo])
     del rank
     return np.concatenate(rows, axis=0)
+
+
+def combine_partials(local, device=None):
+    """All-gather one complex partial per rank and sum them in rank order
+    (fixed order: every rank gets the same bits; an all_reduce's order is
+    the library's choice)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size()
+    t = torch.tensor([complex(local).real, complex(local).imag], dtype=torch.float64)
+    if device is not None:
+        t = t.to(device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    acc = 0j
+    for p in parts:
+        v = p.cpu().numpy()
+        acc += complex(v[0], v[1])
+    return acc
+
+
+def dense_contour_sum_sharded(model, grid, partial_fn=None, device=None):
+    """Dense cross-check sum over the full grid sharded by flat C-order index
+    range across the ranks of the default process group:
+    rank g sums terms [g T / W, (g+1) T / W) with ttp_dense_sum_range and the
+    partials combine in rank order.  ``partial_fn(model, grid, first, count)``
+    overrides the per-rank device sum (the CPU tests use the oracle)."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    lo, hi = shard_range(grid.n_terms, rank, world)
+    if partial_fn is None:
+        from .pricers import dense_partial_sum
+        partial_fn = dense_partial_sum
+    return combine_partials(partial_fn(model, grid, lo, hi - lo), device=device)

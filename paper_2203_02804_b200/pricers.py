@@ -170,6 +170,27 @@ def price_fourier_dense_batch(models, grid, t=0.0, term_cap=DENSE_TERM_CAP):
     return out
 
 
+def dense_partial_sum(model, grid, first, count):
+    """Raw contour sum (no prefactor) over the flat term range [first, first +
+    count) on the device (ttp_dense_sum_range) -> complex."""
+    _require_admissible(grid)
+    torch = _lib.require_device()
+    lib = _lib.load_library()
+    phi = OracleBatch([PhiGridOracle(model, grid)])
+    vhat = OracleBatch([PayoffGridOracle(model, grid, conj=False)])
+    shape = np.full(grid.d, grid.points_per_axis, dtype=np.int32)
+    d_shape = torch.from_numpy(shape).to("cuda")
+    ws_bytes = lib.ttp_dense_workspace(1, grid.n_terms)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    out = (ctypes.c_double * 2)()
+    st = lib.ttp_dense_sum_range(ctypes.byref(phi.struct), ctypes.byref(vhat.struct),
+                                 shape.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                 ctypes.c_void_p(d_shape.data_ptr()), 1, int(first), int(count), out,
+                                 ctypes.c_void_p(ws.data_ptr()), ws_bytes, _lib.stream_handle())
+    _lib.raise_for(st, "dense sum")
+    return complex(out[0], out[1])
+
+
 def price_fourier_dense(model, grid, t=0.0, term_cap=DENSE_TERM_CAP):
     """Dense nested contour sum on the GPU (pricers.py:199-231)."""
     if model.d != grid.d:

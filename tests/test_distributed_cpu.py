@@ -65,3 +65,42 @@ def test_shard_ranges_partition():
             spans = [shard_range(n, r, w) for r in range(w)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def _oracle_range_sum(model, grid, first, count):
+    """CPU stand-in for ttp_dense_sum_range: the oracle's terms over a flat range."""
+    from oracle import ttp_oracle as O
+    gm = O.GridModel(model.r, model.sigma, model.T, model.s0, model.strike, model.corr, grid.n,
+                     grid.eta, grid.alpha)
+    n = grid.points_per_axis
+    flat = np.arange(first, first + count)
+    idx = np.stack(np.unravel_index(flat, (n,) * grid.d), axis=1)
+    return complex(np.sum(gm.phi_oracle()(idx) * np.conj(gm.vhat_oracle()(idx))))
+
+
+def _dense_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    from paper_2203_02804_b200 import configs
+    from paper_2203_02804_b200.distributed import dense_contour_sum_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    spec = configs.CONFIGS[1]
+    m = configs.make_model(1)
+    total = dense_contour_sum_sharded(m, spec.grid, partial_fn=_oracle_range_sum)
+    np.save(out_path + f".{rank}.npy", np.array([total]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_dense_sum(tmp_path):
+    """the dense cross-check split by flat index range over two
+    ranks combines (in rank order, identically on both ranks) to the full sum."""
+    from paper_2203_02804_b200 import configs
+    out = str(tmp_path / "dense")
+    mp.spawn(_dense_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r0, r1 = np.load(out + ".0.npy")[0], np.load(out + ".1.npy")[0]
+    assert r0 == r1
+    spec = configs.CONFIGS[1]
+    full = _oracle_range_sum(configs.make_model(1), spec.grid, 0, spec.grid.n_terms)
+    assert abs(r0 - full) <= 1e-12 * abs(full)

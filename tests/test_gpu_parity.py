@@ -474,3 +474,20 @@ def test_cfg5_big_layout_batch_equals_single():
         b = batch.trains.to_trains()[i]
         for ca, cb in zip(a.cores, b.cores):
             np.testing.assert_array_equal(ca, cb)
+
+
+def test_dense_range_partials_sum_to_full_grid():
+    """ttp_dense_sum_range shards the dense cross-check by flat
+    index range; the shard partials add up to the full-grid sum."""
+    from paper_2203_02804_b200.pricers import dense_partial_sum
+    from paper_2203_02804_b200.distributed import shard_range
+    spec = configs.CONFIGS[2]
+    m = configs.make_model(2)
+    grid = P.GridSpec(n=spec.grid.n // 2, eta=spec.grid.eta, alpha=spec.grid.alpha, d=spec.grid.d)
+    full = dense_partial_sum(m, grid, 0, grid.n_terms)
+    parts = [dense_partial_sum(m, grid, *(lambda lo, hi: (lo, hi - lo))(*shard_range(grid.n_terms, g, 4)))
+             for g in range(4)]
+    assert abs(sum(parts) - full) <= 1e-13 * abs(full)
+    price = P.price_fourier_dense(m, grid).price
+    pref = np.exp(-m.r * m.T) * grid.eta ** grid.d / (2 * np.pi) ** grid.d
+    assert (pref * full).real == pytest.approx(price, rel=1e-14)
