@@ -104,3 +104,50 @@ def test_gloo_world2_sharded_dense_sum(tmp_path):
     spec = configs.CONFIGS[1]
     full = _oracle_range_sum(configs.make_model(1), spec.grid, 0, spec.grid.n_terms)
     assert abs(r0 - full) <= 1e-12 * abs(full)
+
+
+def _split2_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    from oracle import ttp_oracle as O
+    from paper_2203_02804_b200 import CrossConfig, TensorTrain, configs
+    from paper_2203_02804_b200.distributed import price_fourier_tt_split2
+    from paper_2203_02804_b200.oracles import PhiGridOracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def cross_fn(o, shape, cfg):  # CPU restatement in place of the device cross
+        m, g = o.model, o.grid
+        gm = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, g.n, g.eta, g.alpha)
+        f = gm.phi_oracle() if isinstance(o, PhiGridOracle) else gm.vhat_oracle()
+        cores, _ = O.tt_cross(f, shape, cfg.bond_dim, n_conv=cfg.n_conv_samples, seed=cfg.seed)
+        return TensorTrain(cores)
+
+    def inner_fn(bra, ket):
+        return O.tt_inner(list(bra.cores), list(ket.cores))
+
+    spec = configs.CONFIGS[1]
+    cfg = CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed, n_conv_samples=2000)
+    p = price_fourier_tt_split2(configs.make_model(1), spec.grid, cfg, cfg, cross_fn=cross_fn, inner_fn=inner_fn)
+    np.save(out_path + f".{rank}.npy", np.array([p]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_split_crosses():
+    """SURVEY 8(e) optional split: phi on rank 0, vhat on rank 1, cores sent
+    point-to-point, contraction on rank 0, price broadcast; equals the
+    one-process pipeline on the same CPU restatement."""
+    import tempfile
+    from oracle import ttp_oracle as O
+    from paper_2203_02804_b200 import configs
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "split")
+        mp.spawn(_split2_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+        p0, p1 = np.load(out + ".0.npy")[0], np.load(out + ".1.npy")[0]
+    assert p0 == p1
+    spec = configs.CONFIGS[1]
+    m = configs.make_model(1)
+    gm = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, spec.grid.n, spec.grid.eta, spec.grid.alpha)
+    want, _ = O.price_tt(gm, spec.bond_dim, spec.bond_dim, spec.cross_seed, spec.cross_seed, n_conv=2000)
+    assert p0 == pytest.approx(want, rel=1e-13)
