@@ -197,8 +197,13 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128/f64",
         "data": "synthetic (seeded default_rng([4, i]) instances, SURVEY.md 8(d))",
-        "config": {"workload": sp.label, "config_id": CONFIG_ID, "options_per_step": per_step,
-                   "grid_points_per_axis": sp.grid.points_per_axis, "bond_dim": sp.bond_dim},
+        # the GPU arm's workload (same config keys); each reference step is a
+        # bounded sample of it (see cpu_baseline.sample)
+        "config": {"workload": sp.label + f", batch of {args.batch} independent options per GPU per step",
+                   "config_id": CONFIG_ID, "options_per_gpu_per_step": args.batch,
+                   "global_batch": args.batch * world, "grid_points_per_axis": sp.grid.points_per_axis,
+                   "bond_dim": sp.bond_dim, "parallelism": "host cores (rank 0 only)",
+                   "options_timed_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{per_step} config-4 options per step (one per core, 1 BLAS thread "
                                    f"each) on {cpu_model_name()}; the reference is pure Python "
