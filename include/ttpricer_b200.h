@@ -219,6 +219,25 @@ int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const double* d_mats, 
                int64_t max_iters, double rank_tol, int64_t* h_sel, int32_t* h_status,
                void* d_ws, size_t ws_bytes, void* stream);
 
+/* One-call batch pricing (price_fourier_tt, pricers.py:256-294, for n_inst
+ * options sharing grid and configs): the phi cross (PHI_GBM oracle), the
+ * vhat cross (VHAT_MIN oracle, conj_flag 1), the bra-conjugated inner
+ * product and the prefactor, all on `stream`.  h_prefactor[i] =
+ * e^{-r_i (T_i - t)} eta^d / (2 pi)^d.  Outputs: h_price / h_imag (real and
+ * imaginary part of the priced contour sum) per instance, and both crosses'
+ * cores / index sets / reports through out_phi / out_v exactly as
+ * ttp_cross_run.  Instances whose cross failed keep their status in the
+ * out structs and get NaN prices.  The seeded host draws (initial right sets,
+ * convergence samples) come in the two problems, as for ttp_cross_run.      */
+typedef struct ttp_price_problem {
+  ttp_cross_problem phi;
+  ttp_cross_problem vhat;
+  const double* h_prefactor;
+} ttp_price_problem;
+size_t ttp_price_tt_workspace(const ttp_price_problem* prob);
+int ttp_price_tt_batch(const ttp_price_problem* prob, ttp_cross_out* out_phi, ttp_cross_out* out_v,
+                       double* h_price, double* h_imag, void* d_ws, size_t ws_bytes, void* stream);
+
 /* K9: Monte Carlo estimate of the discounted min-option payoff
  * (price_monte_carlo, pricers.py:297-350) for n_inst instances of dimension
  * d, n_samples paths each.  Parameters per instance (doubles, stride

@@ -99,6 +99,14 @@ class CrossProblem(ctypes.Structure):
     ]
 
 
+class PriceProblem(ctypes.Structure):
+    _fields_ = [
+        ("phi", CrossProblem),
+        ("vhat", CrossProblem),
+        ("h_prefactor", ctypes.POINTER(_f64)),
+    ]
+
+
 class CrossLayout(ctypes.Structure):
     _fields_ = [
         ("ranks", _i32 * 65),
@@ -165,6 +173,10 @@ SIGNATURES = [
                             ctypes.POINTER(_f64), _p, _sz, _p]),
     ("ttp_philox4x32", _i32, [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                               ctypes.POINTER(ctypes.c_uint32)]),
+    ("ttp_price_tt_workspace", _sz, [ctypes.POINTER(PriceProblem)]),
+    ("ttp_price_tt_batch", _i32, [ctypes.POINTER(PriceProblem), ctypes.POINTER(CrossOut),
+                                  ctypes.POINTER(CrossOut), ctypes.POINTER(_f64), ctypes.POINTER(_f64),
+                                  _p, _sz, _p]),
     ("ttp_maxvol_workspace", _sz, [_i32, _i64, _i32]),
     ("ttp_maxvol", _i32, [_i32, _i64, _i32, _p, _f64, _i64, _f64, ctypes.POINTER(_i64),
                           ctypes.POINTER(_i32), _p, _sz, _p]),

@@ -248,12 +248,12 @@ def cross_bytes_per_instance(shape, cfg):
     return (ws(2) - ws(1)) + 16 * lay.core_stride + 8 * lay.set_stride
 
 
-def tt_cross_batch(oracles, shape, cfg, with_reports=True):
-    """Batched TT-cross of independent oracles sharing ``shape`` and ``cfg``.
+class _PreparedCross:
+    """Problem + output buffers of one batched cross (shared by tt_cross_batch
+    and the one-call pricer); keeps every buffer the C structs point at alive."""
 
-    Returns a :class:`CrossBatchResult` whose trains stay on the GPU; per
-    instance errors are reported in ``status`` (not raised).
-    """
+
+def _prepare_cross(oracles, shape, cfg):
     torch = _lib.require_device()
     lib = _lib.load_library()
     shape = tuple(int(n) for n in shape)
@@ -293,8 +293,6 @@ def tt_cross_batch(oracles, shape, cfg, with_reports=True):
     )
     if d == 1:
         prob.cfg.bond_dim = 1
-    ws_bytes = lib.ttp_cross_workspace(ctypes.byref(prob))
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     cores = torch.zeros(n * lay.core_stride, dtype=torch.complex128, device=dev)
     left = torch.zeros(n * lay.set_stride, dtype=torch.int32, device=dev)
     right = torch.zeros(n * lay.set_stride, dtype=torch.int32, device=dev)
@@ -313,10 +311,15 @@ def tt_cross_batch(oracles, shape, cfg, with_reports=True):
         h_left_valid=h["lvalid"].ctypes.data_as(P32), h_oracle_calls=h["calls"].ctypes.data_as(P64),
         h_conv_calls=h["ccalls"].ctypes.data_as(P64), h_final_diff=h["diff"].ctypes.data_as(PF),
     )
-    st = lib.ttp_cross_run(ctypes.byref(prob), ctypes.byref(out), ctypes.c_void_p(ws.data_ptr()),
-                           ws_bytes, _lib.stream_handle())
-    _lib.raise_for(st, "tt_cross")
-    del ws
+    pc = _PreparedCross()
+    pc.__dict__.update(prob=prob, out=out, lay=lay, shape=shape, ranks=ranks, cores=cores, left=left,
+                       right=right, h=h, n=n, d=d,
+                       keep=(batch, d_right_init, conv, d_shape, lay, h))
+    return pc
+
+def _finish_cross(pc, with_reports):
+    shape, ranks, cores, n, d, lay, h = pc.shape, pc.ranks, pc.cores, pc.n, pc.d, pc.lay, pc.h
+    left, right = pc.left, pc.right
     trains = DeviceTTBatch(shape, ranks, cores, n)
     if not with_reports:
         return CrossBatchResult(trains, None, h["status"].copy(), h["bond"].copy(), h)
@@ -351,6 +354,23 @@ def tt_cross_batch(oracles, shape, cfg, with_reports=True):
         ))
     return CrossBatchResult(trains, reports, h["status"].copy(), h["bond"].copy(), h)
 
+
+def tt_cross_batch(oracles, shape, cfg, with_reports=True):
+    """Batched TT-cross of independent oracles sharing ``shape`` and ``cfg``.
+
+    Returns a :class:`CrossBatchResult` whose trains stay on the GPU; per
+    instance errors are reported in ``status`` (not raised).
+    """
+    torch = _lib.require_device()
+    lib = _lib.load_library()
+    pc = _prepare_cross(oracles, shape, cfg)
+    ws_bytes = lib.ttp_cross_workspace(ctypes.byref(pc.prob))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=torch.device("cuda"))
+    st = lib.ttp_cross_run(ctypes.byref(pc.prob), ctypes.byref(pc.out), ctypes.c_void_p(ws.data_ptr()),
+                           ws_bytes, _lib.stream_handle())
+    _lib.raise_for(st, "tt_cross")
+    del ws
+    return _finish_cross(pc, with_reports)
 
 def tt_cross(oracle, shape, cfg):
     """Tensor-train approximation of a device oracle (cross.py:358-453).

@@ -651,3 +651,64 @@ extern "C" int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const doubl
   for (int i = 0; i < n_mat; ++i) h_status[i] = stat[i];
   return TTP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// One-call batch pricing: phi cross, vhat cross, inner product, prefactor.
+extern "C" size_t ttp_price_tt_workspace(const ttp_price_problem* prob) {
+  if (!prob) return 0;
+  const size_t a = ttp_cross_workspace(&prob->phi), b = ttp_cross_workspace(&prob->vhat);
+  return (a > b ? a : b) + 256 + 16 * (size_t)(prob->phi.n_inst > 0 ? prob->phi.n_inst : 1);
+}
+
+extern "C" int ttp_price_tt_batch(const ttp_price_problem* prob, ttp_cross_out* out_phi, ttp_cross_out* out_v,
+                                  double* h_price, double* h_imag, void* d_ws, size_t ws_bytes,
+                                  void* stream) {
+  if (!prob || !out_phi || !out_v || !h_price || !h_imag || !prob->h_prefactor)
+    return ttp_fail(TTP_ERR_INVALID, "price_tt_batch: null argument");
+  const ttp_cross_problem& P = prob->phi;
+  const ttp_cross_problem& V = prob->vhat;
+  if (P.d != V.d || P.n_inst != V.n_inst || P.oracle.kind != TTP_ORACLE_PHI_GBM ||
+      V.oracle.kind != TTP_ORACLE_VHAT_MIN)
+    return ttp_fail(TTP_ERR_INVALID, "price_tt_batch: expects a PHI_GBM and a VHAT_MIN problem of one batch");
+  for (int k = 0; k < P.d; ++k)
+    if (P.h_shape[k] != V.h_shape[k]) return ttp_fail(TTP_ERR_INVALID, "price_tt_batch: shape mismatch");
+  if (ws_bytes < ttp_price_tt_workspace(prob))
+    return ttp_fail(TTP_ERR_WORKSPACE, "price_tt_batch: workspace too small");
+  const int n = P.n_inst, d = P.d;
+  if (n == 0) return TTP_OK;
+  const size_t cross_ws = ws_bytes - 256 - 16 * (size_t)n;
+  int st = ttp_cross_run(&P, out_phi, d_ws, cross_ws, stream);
+  if (st != TTP_OK) return st;
+  st = ttp_cross_run(&V, out_v, d_ws, cross_ws, stream);
+  if (st != TTP_OK) return st;
+  ttp_cross_layout Lp, Lv;
+  if (ttp_cross_layout_of(d, P.h_shape, P.cfg.bond_dim, &Lp) != TTP_OK ||
+      ttp_cross_layout_of(d, V.h_shape, V.cfg.bond_dim, &Lv) != TTP_OK)
+    return ttp_fail(TTP_ERR_INVALID, "price_tt_batch: bad layout");
+  ttp_tt_batch bra{}, ket{};
+  bra.d = ket.d = d;
+  bra.n_inst = ket.n_inst = n;
+  bra.h_shape = V.h_shape;
+  ket.h_shape = P.h_shape;
+  bra.h_bonds = Lv.ranks;
+  ket.h_bonds = Lp.ranks;
+  bra.h_offsets = Lv.core_offsets;
+  ket.h_offsets = Lp.core_offsets;
+  bra.stride = Lv.core_stride;
+  ket.stride = Lp.core_stride;
+  bra.d_cores = out_v->d_cores;
+  ket.d_cores = out_phi->d_cores;
+  double* d_raw = reinterpret_cast<double*>(static_cast<unsigned char*>(d_ws) + cross_ws + 128);
+  st = ttp_tt_inner(&bra, &ket, d_raw, stream);
+  if (st != TTP_OK) return st;
+  std::vector<double> raw(2 * (size_t)n);
+  TTP_CUDA_CHECK(cudaMemcpyAsync(raw.data(), d_raw, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost,
+                                 (cudaStream_t)stream));
+  TTP_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+  for (int i = 0; i < n; ++i) {
+    const bool ok = out_phi->h_status[i] == TTP_OK && out_v->h_status[i] == TTP_OK;
+    h_price[i] = ok ? prob->h_prefactor[i] * raw[2 * i] : NAN;
+    h_imag[i] = ok ? prob->h_prefactor[i] * raw[2 * i + 1] : NAN;
+  }
+  return TTP_OK;
+}

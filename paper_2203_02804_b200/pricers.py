@@ -326,6 +326,49 @@ def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference=
     return results
 
 
+def price_fourier_tt_batch_capi(models, grid, cfg_phi, cfg_v, t=0.0):
+    """price_fourier_tt_batch through the single C entry point
+    ttp_price_tt_batch (both crosses, the inner product and the prefactor in
+    one call) -- the binding a non-Python host would use.
+    Same prices as price_fourier_tt_batch; returns a list of PricingResult."""
+    from .cross import _finish_cross, _prepare_cross
+    for m in models:
+        if m.d != grid.d:
+            raise ValueError(f"model has d={m.d} but grid has d={grid.d}")
+    _require_admissible(grid)
+    torch = _lib.require_device()
+    lib = _lib.load_library()
+    start = time.perf_counter()
+    shape = (grid.points_per_axis,) * grid.d
+    pp = _prepare_cross(OracleBatch([PhiGridOracle(m, grid) for m in models]), shape, cfg_phi)
+    pv = _prepare_cross(OracleBatch([PayoffGridOracle(m, grid, conj=True) for m in models]), shape, cfg_v)
+    pref = np.array([_prefactor(m, grid, t) for m in models], dtype=np.float64)
+    prob = _lib.PriceProblem(phi=pp.prob, vhat=pv.prob,
+                             h_prefactor=pref.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    ws_bytes = lib.ttp_price_tt_workspace(ctypes.byref(prob))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+    n = len(models)
+    price = np.zeros(n)
+    imag = np.zeros(n)
+    st = lib.ttp_price_tt_batch(ctypes.byref(prob), ctypes.byref(pp.out), ctypes.byref(pv.out),
+                                price.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                imag.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                ctypes.c_void_p(ws.data_ptr()), ws_bytes, _lib.stream_handle())
+    _lib.raise_for(st, "price_tt_batch")
+    del ws
+    rp, rv = _finish_cross(pp, True), _finish_cross(pv, True)
+    wall = time.perf_counter() - start
+    out = []
+    for i in range(n):
+        err = rp.error_for(i) or rv.error_for(i)
+        if err is not None:
+            raise err
+        out.append(PricingResult(float(price[i]), "fourier_tt", wall / n, {
+            "cross_phi": rp.reports[i], "cross_v": rv.reports[i], "imag_part": float(imag[i]),
+            "oracle_calls_total": rp.reports[i].oracle_calls + rv.reports[i].oracle_calls}))
+    return out
+
+
 def price_fourier_tt(model, grid, cfg_phi, cfg_v, t=0.0, dense_reference="auto",
                      term_cap=DENSE_TERM_CAP):
     """Tensor-train contraction of the contour sum (pricers.py:256-294)."""

@@ -491,3 +491,18 @@ def test_dense_range_partials_sum_to_full_grid():
     price = P.price_fourier_dense(m, grid).price
     pref = np.exp(-m.r * m.T) * grid.eta ** grid.d / (2 * np.pi) ** grid.d
     assert (pref * full).real == pytest.approx(price, rel=1e-14)
+
+
+def test_one_call_c_api_equals_python_orchestration():
+    """ttp_price_tt_batch (both crosses + inner product + prefactor in one C
+    call) prices bitwise like the Python-orchestrated batch."""
+    from paper_2203_02804_b200.pricers import price_fourier_tt_batch_capi
+    spec = configs.CONFIGS[2]
+    models = [configs.make_model(2, i) for i in range(6)]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    a = P.price_fourier_tt_batch(models, spec.grid, cfg, cfg)
+    b = price_fourier_tt_batch_capi(models, spec.grid, cfg, cfg)
+    for x, y in zip(a, b):
+        assert x.price == y.price
+        assert x.diagnostics["imag_part"] == y.diagnostics["imag_part"]
+        assert x.diagnostics["cross_phi"].to_dict() == y.diagnostics["cross_phi"].to_dict()
