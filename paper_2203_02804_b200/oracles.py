@@ -173,16 +173,26 @@ class OracleBatch:
         if not oracles:
             raise ValueError("empty oracle batch")
         first = oracles[0]
-        for o in oracles[1:]:
-            if not first.compatible(o):
+        plist = [o.params() for o in oracles]
+        tlist = [o.table() for o in oracles]
+        # layout check (per-instance payloads computed once; the table
+        # layouts only exist for the table-backed kinds)
+        table_kind = first.kind in (_lib.ORACLE_SEPARABLE, _lib.ORACLE_TT, _lib.ORACLE_TABLE)
+        off0, bonds0 = first.table_offsets(), first.tt_bonds()
+        for o, p, t in zip(oracles[1:], plist[1:], tlist[1:]):
+            same = (type(o) is type(first) and o.d == first.d and p.shape == plist[0].shape
+                    and t.shape == tlist[0].shape)
+            if same and table_kind:
+                same = np.array_equal(o.table_offsets(), off0) and np.array_equal(o.tt_bonds(), bonds0)
+            if not same:
                 raise ValueError("oracles in one batch must share kind and layout")
         torch = _lib.require_device()
         self.kind = first.kind
         self.d = first.d
         self.n_inst = len(oracles)
         dev = torch.device("cuda")
-        params = np.stack([o.params() for o in oracles]).astype(np.float64)
-        table = np.stack([o.table() for o in oracles]).astype(np.complex128)
+        params = np.stack(plist).astype(np.float64)
+        table = np.stack(tlist).astype(np.complex128)
         self._params = torch.from_numpy(np.ascontiguousarray(params)).to(dev)
         self._table = torch.from_numpy(np.ascontiguousarray(table)).to(dev)
         self._offsets = torch.from_numpy(first.table_offsets().astype(np.int64)).to(dev)
