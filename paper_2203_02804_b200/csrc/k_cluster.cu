@@ -67,6 +67,7 @@ constexpr int CT = CLUSTER_THREADS;
 constexpr int CW = CT / 32;
 constexpr int RMAX = 64;
 constexpr int QX_ROWS = 64;  // rows per staged tile of the DMMA Q*X products
+__constant__ int g_serpentine = 1;  // dev knob (A/B of the serpentine row order)
 
 struct __align__(16) Rec {
   double v;
@@ -148,6 +149,16 @@ __device__ __forceinline__ const cplx* Qrow(const CC& c, int g) { return c.Qg + 
 // independent loads before the dependent FMAs keeps KB loads in flight per
 // warp instead of one.  Accumulation order is unchanged (t ascending).
 constexpr int KB = 8;
+
+// Serpentine row passes: this thread's rows (l = tid + k CT) in ascending
+// (rev = false) or descending order.  Consecutive passes over a slice run in
+// opposite directions, so each pass starts on the lines the previous one
+// touched last -- still in L2 when the working set (74 instances' slices)
+// exceeds the L2 -- instead of on the ones evicted first.  Only used for
+// passes whose per-row work is order independent.
+#define FOR_MY_ROWS(l, nl, rev)                                                \
+  for (int _k = 0, _nk = ((nl) + CT - 1) / CT; _k < _nk; ++_k)                 \
+    if (const int l = threadIdx.x + ((rev) ? (_nk - 1 - _k) : _k) * CT; l < (nl))
 
 // sum_t conj(S[t]) * W(l, t), t in [t0, r)
 __device__ __forceinline__ cplx row_dotc(const CC& c, const cplx* S, int l, int t0, int r) {
@@ -743,8 +754,8 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
     par ^= 1;
     __syncthreads();
     SP(spt, 3);
-    // local update of my rows
-    for (int l = threadIdx.x; l < nl; l += CT) {
+    // local update of my rows (descending: the partials pass ran ascending)
+    FOR_MY_ROWS(l, nl, g_serpentine) {
       const int g = lo + l;
       if (g < i) continue;
       if (g == i) {
@@ -1323,7 +1334,7 @@ __device__ void start_pair_s(cg::cluster_group& cl, CC& c, int& par) {
   for (int k = 0; k < r; ++k) {
     // ---- row pass: downdate with step k-1 (QRCP), Schur column k (LU)
     Cand a1{-1.0, LLONG_MAX, -1}, a2{-1.0, LLONG_MAX, -1};
-    for (int l = threadIdx.x; l < nl; l += CT) {
+    FOR_MY_ROWS(l, nl, g_serpentine && (k & 1)) {
       const int p1 = c.rpos[l], p2 = c.rpos2[l];
       const bool dd = (k > 0 && p1 > k - 1);
       const bool lu = (p2 >= k);
@@ -1574,7 +1585,7 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
     if (threadIdx.x == 0) c.sel[j] = i;
     SP(spt, 12);
     a = Cand{-1.0, LLONG_MAX, -1};
-    for (int l = threadIdx.x; l < nl; l += CT) {
+    FOR_MY_ROWS(l, nl, g_serpentine && ((it & 1) == 0)) {
       const cplx blj = Wl(c, l, j);
       cplx* p = c.Ws + l;
       const long long ld = c.ldw;
