@@ -593,7 +593,7 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
   // (5) Q(g, b) = delta(g, b) - sum_{a <= b} V(g, a) M(a, b), written to Qg
   //     in logical column order; outputs in blocks of 8 per row thread.
   constexpr int OB = 8;
-  for (int l = threadIdx.x; l < nl; l += CT) {
+  FOR_MY_ROWS(l, nl, g_serpentine) {  // the Gram pass ran ascending
     const int g = lo + l;
     for (int b0 = 0; b0 < r; b0 += OB) {
       cplx acc[OB];
@@ -1334,7 +1334,7 @@ __device__ void start_pair_s(cg::cluster_group& cl, CC& c, int& par) {
   for (int k = 0; k < r; ++k) {
     // ---- row pass: downdate with step k-1 (QRCP), Schur column k (LU)
     Cand a1{-1.0, LLONG_MAX, -1}, a2{-1.0, LLONG_MAX, -1};
-    FOR_MY_ROWS(l, nl, g_serpentine && (k & 1)) {
+    FOR_MY_ROWS(l, nl, g_serpentine && ((k & 1) == 0)) {  // the norm pass before round 0 ran ascending
       const int p1 = c.rpos[l], p2 = c.rpos2[l];
       const bool dd = (k > 0 && p1 > k - 1);
       const bool lu = (p2 >= k);
