@@ -1590,12 +1590,13 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
       cplx* p = c.Ws + l;
       const long long ld = c.ldw;
       int t = 0;
-      for (; t + KB <= r; t += KB) {
-        cplx x[KB];
+      constexpr int KS = 2 * KB;  // the swap pass is the hottest loop: 16 loads in flight
+      for (; t + KS <= r; t += KS) {
+        cplx x[KS];
 #pragma unroll
-        for (int q = 0; q < KB; ++q) x[q] = p[(t + q) * ld];
+        for (int q = 0; q < KS; ++q) x[q] = p[(t + q) * ld];
 #pragma unroll
-        for (int q = 0; q < KB; ++q) {
+        for (int q = 0; q < KS; ++q) {
           const cplx v = cfma(blj, w[t + q], x[q]);
           p[(t + q) * ld] = v;
           const Cand b{cabs2(v), (long long)(lo + l) * r + t + q, l};
