@@ -1348,12 +1348,13 @@ __device__ void start_pair_s(cg::cluster_group& cl, CC& c, int& par) {
       const cplx* q = Qrow(c, lo + l);
       cplx t1 = mk(0.0, 0.0), s2 = mk(0.0, 0.0);
       int t = 0;
-      for (; t + KB <= r; t += KB) {
-        cplx x[KB];
+      constexpr int KS = 2 * KB;  // 16 loads in flight per thread
+      for (; t + KS <= r; t += KS) {
+        cplx x[KS];
 #pragma unroll
-        for (int qq = 0; qq < KB; ++qq) x[qq] = q[(long long)(t + qq) * m];
+        for (int qq = 0; qq < KS; ++qq) x[qq] = q[(long long)(t + qq) * m];
 #pragma unroll
-        for (int qq = 0; qq < KB; ++qq) {
+        for (int qq = 0; qq < KS; ++qq) {
           t1 = cfma(u[t + qq], x[qq], t1);
           if (t + qq < k) s2 = cfma(x[qq], w2[t + qq], s2);
           else if (t + qq == k) s2 = csub(x[qq], s2);
