@@ -762,9 +762,22 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
         Wl(c, l, ci) = mk(h.beta, 0.0);
         for (int q = 1; q <= ntr; ++q) Wl(c, l, c.colmap[i + q]) = c.vec2[q - 1];
       } else if (!ident) {
-        const cplx x = cmul(Wl(c, l, ci), scal);
-        Wl(c, l, ci) = x;
-        row_sub_cols(c, c.colmap + i + 1, c.vec, x, l, ntr);
+        // issue the pivot entry and the first KB trailing entries together
+        // (the store of the new pivot entry would otherwise order the
+        // trailing loads after the pivot load's round trip)
+        cplx* prow = c.Ws + l;
+        const long long ld = c.ldw;
+        const int* cols = c.colmap + i + 1;
+        const int n0 = min(ntr, KB);
+        cplx y[KB];
+#pragma unroll
+        for (int u = 0; u < KB; ++u) y[u] = (u < n0) ? prow[cols[u] * ld] : mk(0.0, 0.0);
+        const cplx x = cmul(prow[(long long)ci * ld], scal);
+#pragma unroll
+        for (int u = 0; u < KB; ++u)
+          if (u < n0) prow[cols[u] * ld] = csub(y[u], cmul(x, c.vec[u]));
+        prow[(long long)ci * ld] = x;
+        if (ntr > n0) row_sub_cols(c, cols + n0, c.vec + n0, x, l, ntr - n0);
       }
     }
     __syncthreads();
