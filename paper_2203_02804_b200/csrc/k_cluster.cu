@@ -263,16 +263,27 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
   t.sel = (int*)take(sizeof(int) * r);
   t.best = (int*)take(sizeof(int) * r);
   t.starts = (int*)take(sizeof(int) * 2 * r);
-  t.vn1 = big ? nullptr : (double*)take(sizeof(double) * ldw);
-  t.vn2 = big ? nullptr : (double*)take(sizeof(double) * ldw);
-  t.rpos = big ? nullptr : (int*)take(sizeof(int) * ldw);
+  // The starts' per-row state (vn1, vn2, rpos, rpos2) and the staged Q row
+  // tile of the DMMA Q*X products (form_B / the factor, global-slice mode,
+  // r <= 32) are never live together: they share one region, which keeps
+  // the carve (and so the L1 the row passes lose to shared memory) small.
+  {
+    const size_t a8 = (sizeof(double) * (size_t)ldw + 15) & ~(size_t)15;
+    const size_t a4 = (sizeof(int) * (size_t)ldw + 15) & ~(size_t)15;
+    const size_t rows_bytes = big ? 0 : 2 * a8 + 2 * a4;
+    const size_t qt_bytes = (global_slice && r <= 32)
+                                ? sizeof(double) * QX_ROWS * (size_t)(((2 * r + 3) & ~3) + 4) : 0;
+    unsigned char* u = (unsigned char*)take(rows_bytes > qt_bytes ? rows_bytes : qt_bytes);
+    t.vn1 = big ? nullptr : (double*)u;
+    t.vn2 = big ? nullptr : (double*)(u ? u + a8 : nullptr);
+    t.rpos = big ? nullptr : (int*)(u ? u + 2 * a8 : nullptr);
+    t.rpos2 = big ? nullptr : (int*)(u ? u + 2 * a8 + a4 : nullptr);
+    t.qtile = qt_bytes ? (double*)u : nullptr;
+  }
   t.rec = (Rec*)take(sizeof(Rec) * 2);
   t.wrec = (WCand*)take(sizeof(WCand) * 2 * CW);
   t.wrec2 = (WCand*)take(sizeof(WCand) * 2 * CW);
-  t.rpos2 = big ? nullptr : (int*)take(sizeof(int) * ldw);
   t.sp = (cplx*)take(sizeof(cplx) * 8 * r);
-  // staged Q row tile of the DMMA Q*X products (global-slice mode, r <= 32)
-  t.qtile = (global_slice && r <= 32) ? (double*)take(sizeof(double) * QX_ROWS * (((2 * r + 3) & ~3) + 4)) : nullptr;
   t.wrow = (cplx*)take(sizeof(cplx) * 2 * CW * r);
   t.wcand = (Cand*)take(sizeof(Cand) * CW);
   t.wss = (Ssq*)take(sizeof(Ssq) * CW);
