@@ -272,7 +272,7 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
     const size_t a4 = (sizeof(int) * (size_t)ldw + 15) & ~(size_t)15;
     const size_t rows_bytes = big ? 0 : 2 * a8 + 2 * a4;
     const size_t qt_bytes = (global_slice && r <= 32)
-                                ? sizeof(double) * QX_ROWS * (size_t)(((2 * r + 3) & ~3) + 4) : 0;
+                                ? 2 * sizeof(double) * QX_ROWS * (size_t)(((2 * r + 3) & ~3) + 4) : 0;
     unsigned char* u = (unsigned char*)take(rows_bytes > qt_bytes ? rows_bytes : qt_bytes);
     t.vn1 = big ? nullptr : (double*)u;
     t.vn2 = big ? nullptr : (double*)(u ? u + a8 : nullptr);
@@ -926,21 +926,38 @@ __device__ void qx_dmma(const CC& c, const cplx* X, int ldx, Sink sink) {
     }
     breg[ks] = b;
   }
-  double* tile = c.qtile;
-  for (int e = threadIdx.x; e < QX_ROWS * (Kp - 2 * r); e += CT) {
-    const int row = e / (Kp - 2 * r), k = 2 * r + (e - row * (Kp - 2 * r));
-    tile[row * ldA + k] = 0.0;
+  // two staging buffers: the Q row tile of step t+1 streams in (cp.async)
+  // while step t runs on the tensor cores
+  double* tiles[2] = {c.qtile, c.qtile + QX_ROWS * ldA};
+  __syncthreads();  // the region is shared with the starts' per-row state
+  for (int e = threadIdx.x; e < 2 * QX_ROWS * (Kp - 2 * r); e += CT) {
+    const int bb = e / (QX_ROWS * (Kp - 2 * r)), e2 = e - bb * QX_ROWS * (Kp - 2 * r);
+    const int row = e2 / (Kp - 2 * r), k = 2 * r + (e2 - row * (Kp - 2 * r));
+    tiles[bb][row * ldA + k] = 0.0;
   }
-  for (int l0 = 0; l0 < nl; l0 += QX_ROWS) {
-    __syncthreads();
+  // rows past nl are zero-filled by cp.async with a 0-byte source
+  auto issue = [&](int l0, double* dst) {
     for (int e = threadIdx.x; e < QX_ROWS * r; e += CT) {
       const int t = e / QX_ROWS, row = e - t * QX_ROWS;
       const int l = l0 + row;
-      const cplx v = (l < nl) ? c.Qg[(long long)t * m + lo + l] : mk(0.0, 0.0);
-      tile[row * ldA + 2 * t] = v.x;
-      tile[row * ldA + 2 * t + 1] = v.y;
+      const cplx* src = c.Qg + (long long)t * m + lo + min(l, nl - 1);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + row * ldA + 2 * t);
+      const int bytes = (l < nl) ? 16 : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(bytes));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  issue(0, tiles[0]);
+  int buf = 0;
+  for (int l0 = 0; l0 < nl; l0 += QX_ROWS, buf ^= 1) {
+    if (l0 + QX_ROWS < nl) {
+      issue(l0 + QX_ROWS, tiles[buf ^ 1]);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
     }
     __syncthreads();
+    const double* tile = tiles[buf];
     if (active) {
       for (int mi = mgrp; mi < QX_ROWS / 8; mi += MG) {
         const int m0 = mi * 8;
@@ -957,8 +974,8 @@ __device__ void qx_dmma(const CC& c, const cplx* X, int ldx, Sink sink) {
         if (l < nl && j < r) sink(l, j, mk(c0, c1));
       }
     }
+    __syncthreads();  // tile buf is refilled by the issue two steps later
   }
-  __syncthreads();
 }
 
 // B = Q X for my rows (into Ws) and for the selected rows (selb); returns my
