@@ -39,9 +39,10 @@ for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
     print(f"cfg{cid} batch {nb}: wall {wall * 1e3:.1f} ms; bond kernel {st['bond_kernel'][2]:.2f} ms / "
           f"{st['bond_kernel'][0]} launches; conv {st['conv_site_kernel'][2]:.2f} ms; last bond phases: "
           + " ".join(marks) + f"; total {(clk[8] - clk[0]) / ghz / 1e3:.1f}us", flush=True)
-    sub = ["pivot+recomp", "partials", "clsync", "reduce", "update", "-", "zung2r"]
+    sub = ["pivot+recomp", "partials", "clsync", "reduce", "update", "wy.gram", "wy.exchange"]
     print("    colbasis sub-phases (all bonds of the sweep): " + " ".join(
-        f"{sub[k]}={out[16 + k] / ghz / 1e3:.1f}us" for k in range(7)), flush=True)
+        f"{sub[k]}={out[16 + k] / ghz / 1e3:.1f}us" for k in range(7))
+        + f" wy.T={out[16 + 14] / ghz / 1e3:.1f}us wy.M+sync={out[16 + 15] / ghz / 1e3:.1f}us", flush=True)
     sub2 = ["sw.publish", "sw.clsync", "sw.winner", "sw.barrier", "sw.selb", "sw.rowpass"]
     print("    swap sub-phases (all bonds, both runs): " + " ".join(
         f"{sub2[k]}={out[24 + k] / ghz / 1e3:.1f}us" for k in range(6)), flush=True)
