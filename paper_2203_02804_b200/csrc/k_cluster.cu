@@ -498,6 +498,7 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
   cplx* X = c.aug;          // this CTA's packed partials (read remotely)
   cplx* P = c.aug + r * r;  // reduced: strict upper = V^H V, strict lower = V1
   cplx* T = c.selb;         // r x r row-major, upper triangular
+  SP_BEGIN(spw);
   // (1) Gram partials over local rows, 4 x 4 tiles (upper tile triangle),
   //     lanes stride rows (coalesced column reads), one warp per tile.
   constexpr int TB = 4;
@@ -560,6 +561,7 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
     if (a > b) X[e] = (a >= lo && a < lo + nl) ? Wl(c, a - lo, c.colmap[b]) : mk(0.0, 0.0);
   }
   cl.sync();
+  SP(spw, 5);
   // (2) fixed rank order sum, identical in every CTA
   for (int e = threadIdx.x; e < r * r; e += CT) {
     const int a = e / r, b = e - a * r;
@@ -569,6 +571,7 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
     P[e] = s;
   }
   __syncthreads();
+  SP(spw, 6);
   // (3) zlarft (forward, columnwise): T(i,i) = tau_i,
   //     T(0:i, i) = -tau_i T(0:i, 0:i) G(0:i, i).  Lane owns rows of T.
   if (warp == 0) {
@@ -588,6 +591,7 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
     }
   }
   cl.sync();  // every CTA finished reading the remote partials in X
+  SP(spw, 14);
   // (4) M = T V1^H (upper triangular) into X
   cplx* M = X;
   for (int e = threadIdx.x; e < r * r; e += CT) {
@@ -601,6 +605,7 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
     M[e] = s;
   }
   __syncthreads();
+  SP(spw, 15);
   // (5) Q(g, b) = delta(g, b) - sum_{a <= b} V(g, a) M(a, b), written to Qg
   //     in logical column order; outputs in blocks of 8 per row thread.
   constexpr int OB = 8;
