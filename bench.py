@@ -311,7 +311,9 @@ def main():
         lay = _Layout(shape, sp.bond_dim)
         nb = len(models)
         h2d = nb * 8 * ((3 + d + d * d) + 5) + 2 * (lay.set_stride * 4 + 4 * d)
-        d2h = nb * (16 + 2 * 2 * lay.set_stride * 4 + 2 * (4 * 5 + 8 * 3) + 8)
+        # prices (complex) + per-instance cross counters of both crosses; the
+        # index sets stay on the device until a report's sets are read
+        d2h = nb * (16 + 2 * (4 * 5 + 8 * 3) + 8)
         e2e = {"value": n_total * args.steps / float(e_el.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 

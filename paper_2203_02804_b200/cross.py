@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -317,14 +318,31 @@ def _prepare_cross(oracles, shape, cfg):
                        keep=(batch, d_right_init, conv, d_shape, lay, h))
     return pc
 
+class _LazyHost:
+    """A device tensor copied to a host array on first use (then cached)."""
+
+    def __init__(self, t, shape):
+        self._t, self._shape, self._a = t, shape, None
+        self._lock = threading.Lock()
+
+    def get(self):
+        with self._lock:
+            if self._a is None:
+                self._a = self._t.cpu().numpy().reshape(self._shape)
+                self._t = None
+            return self._a
+
+
 def _finish_cross(pc, with_reports):
     shape, ranks, cores, n, d, lay, h = pc.shape, pc.ranks, pc.cores, pc.n, pc.d, pc.lay, pc.h
     left, right = pc.left, pc.right
     trains = DeviceTTBatch(shape, ranks, cores, n)
     if not with_reports:
         return CrossBatchResult(trains, None, h["status"].copy(), h["bond"].copy(), h)
-    left_h = left.cpu().numpy().reshape(n, lay.set_stride)
-    right_h = right.cpu().numpy().reshape(n, lay.set_stride)
+    # the packed index sets stay on the device until a report's sets are
+    # first read (most callers only read prices and counters)
+    left_h = _LazyHost(left, (n, lay.set_stride))
+    right_h = _LazyHost(right, (n, lay.set_stride))
     total = math.prod(shape)
     reports = []
     lvalid = h["lvalid"].reshape(n, d + 1)
@@ -332,13 +350,13 @@ def _finish_cross(pc, with_reports):
     def left_of(i):
         if d == 1:
             return lambda: [[()], None]
-        return lambda: ([[()]] + [lay.unpack_set(left_h[i], k, k) if lvalid[i, k] else None
+        return lambda: ([[()]] + [lay.unpack_set(left_h.get()[i], k, k) if lvalid[i, k] else None
                                   for k in range(1, d)] + [None])
 
     def right_of(i):
         if d == 1:
             return lambda: [None, [()]]
-        return lambda: [None] + [lay.unpack_set(right_h[i], k, d - k) for k in range(1, d)] + [[()]]
+        return lambda: [None] + [lay.unpack_set(right_h.get()[i], k, d - k) for k in range(1, d)] + [[()]]
 
     for i in range(n):
         lsets, rsets = left_of(i), right_of(i)
