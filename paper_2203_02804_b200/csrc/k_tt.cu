@@ -16,6 +16,7 @@
 //        of once per sample.
 #include "ttp_internal.h"
 #include "launch.h"
+#include <cstring>
 
 namespace {
 
@@ -184,6 +185,167 @@ tt_inner_staged_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out,
     __syncthreads();
   }
   if (tid == 0) out[inst] = env[0];
+}
+
+// FP64 tensor-core variant (DMMA m8n8k4) working on chunks of IC_SC values
+// of s at a time, so each of the two GEMMs per chunk is large enough to keep
+// the tensor pipe busy between barriers:
+//   T  = env K[:, chunk, :]                  (Db x Dk)(Dk x SC*Dk2)
+//   E += sum_{a, s in chunk} conj(B[a,s,:])^T T[a,s,:]   (K dim = Db*SC)
+// as real GEMMs on the interleaved layout (left operands as stored, with the
+// conjugate sign for B; right operands expanded on the fly).  E lives in the
+// DMMA accumulators for the whole site.  Core slices of the next chunk stream
+// in by cp.async while the current one is contracted.  Bonds <= 32.
+constexpr int IC_SC = 2;
+constexpr int IC_THREADS = 512;
+
+__device__ __forceinline__ void ic_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// expanded right operand G'[k][n] of a complex matrix (rows x cols, ld ldg)
+__device__ __forceinline__ double ic_gexp(const cplx* G, int ldg, int rows, int cols, int k, int n) {
+  const int a = k >> 1, c = n >> 1;
+  if (a >= rows || c >= cols) return 0.0;
+  const cplx g = G[a * ldg + c];
+  return ((k & 1) == (n & 1)) ? g.x : ((n & 1) ? g.y : -g.y);
+}
+
+__global__ void __launch_bounds__(IC_THREADS, 1)
+tt_inner_chunk_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) {
+  extern __shared__ __align__(16) cplx sm[];
+  constexpr int MX = 32;
+  const int inst = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  constexpr int NW = IC_THREADS / 32;
+  const int ldE = 2 * MX + 4;
+  double* envd = reinterpret_cast<double*>(sm);                 // MX x ldE
+  cplx* T = reinterpret_cast<cplx*>(envd + MX * ldE);            // MX x SC*MX
+  cplx* stage = T + MX * IC_SC * MX;                             // [2] x (Kc + Bc)
+  const int selems = 2 * MX * IC_SC * MX;
+  for (int e = threadIdx.x; e < MX * ldE; e += IC_THREADS) envd[e] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) envd[0] = 1.0;
+  __syncthreads();
+  for (int k = 0; k < bra.d; ++k) {
+    const int Db = bra.bonds[k], Db2 = bra.bonds[k + 1];
+    const int Dk = ket.bonds[k], Dk2 = ket.bonds[k + 1];
+    const int n = bra.shape[k];
+    const cplx* B = bra.cores + inst * bra.stride + bra.off[k];
+    const cplx* K = ket.cores + inst * ket.stride + ket.off[k];
+    const int nch = (n + IC_SC - 1) / IC_SC;
+    const int ldK = IC_SC * Dk2, ldB = IC_SC * Db2;
+    // chunk staging: Kc[b][sl*Dk2 + c], Bc[a][sl*Db2 + a2]; missing sl zero-filled
+    auto issue = [&](int ch, int buf) {
+      cplx* Kc = stage + buf * selems;
+      cplx* Bc = Kc + MX * IC_SC * MX;
+      const int s0 = ch * IC_SC;
+      for (int e = threadIdx.x; e < Dk * ldK; e += IC_THREADS) {
+        const int b = e / ldK, j = e - b * ldK, sl = j / Dk2, c = j - sl * Dk2;
+        const bool ok = s0 + sl < n;
+        const cplx* src = K + ((long long)b * n + (ok ? s0 + sl : 0)) * Dk2 + c;
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(Kc + e);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0));
+      }
+      for (int e = threadIdx.x; e < Db * ldB; e += IC_THREADS) {
+        const int a = e / ldB, j = e - a * ldB, sl = j / Db2, c = j - sl * Db2;
+        const bool ok = s0 + sl < n;
+        const cplx* src = B + ((long long)a * n + (ok ? s0 + sl : 0)) * Db2 + c;
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(Bc + e);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0));
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    // GEMM2 output tiles: n-tile (warp & 7) of 2*Dk2, m-tiles (warp >> 3) + 2i of Db2
+    const int ntn2 = (2 * Dk2 + 7) / 8, mtn2 = (Db2 + 7) / 8;
+    const int nt2 = warp & 7, mg2 = warp >> 3;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    issue(0, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+      const int buf = ch & 1;
+      if (ch + 1 < nch) {
+        issue(ch + 1, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;\n" ::);
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+      }
+      __syncthreads();
+      const cplx* Kc = stage + buf * selems;
+      const cplx* Bc = Kc + MX * IC_SC * MX;
+      // ---- GEMM1: T = env Kc   (rows Db, real cols 2*ldK, K' = 2 Dk)
+      {
+        const int ntn1 = (2 * ldK + 7) / 8, mtn1 = (Db + 7) / 8, ks1 = (2 * Dk + 3) / 4;
+        for (int nt = warp; nt < ntn1; nt += NW) {
+          double c1[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+          for (int kk = 0; kk < ks1; ++kk) {
+            const int kx = 4 * kk + tig;
+            const double bv = ic_gexp(Kc, ldK, Dk, ldK, kx, nt * 8 + gid);
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+              if (mt < mtn1) {
+                const int row = mt * 8 + gid;
+                const double av = (row < Db && kx < 2 * Dk) ? envd[row * ldE + kx] : 0.0;
+                ic_dmma(c1[mt][0], c1[mt][1], av, bv);
+              }
+            }
+          }
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            const int row = mt * 8 + gid, col = (nt * 8 + 2 * tig) >> 1;
+            if (mt < mtn1 && row < Db && col < ldK) T[row * ldK + col] = mk(c1[mt][0], c1[mt][1]);
+          }
+        }
+      }
+      __syncthreads();
+      // ---- GEMM2: E += Bc^H T   (K dim kappa = a*SC + sl, T rows kappa)
+      if (nt2 < ntn2) {
+        const int kdim = Db * IC_SC, ks2 = (2 * kdim + 3) / 4;
+        for (int kk = 0; kk < ks2; ++kk) {
+          const int kx = 4 * kk + tig;
+          const int kap = kx >> 1;
+          const int a = kap / IC_SC, sl = kap - a * IC_SC;
+          const double bv = ic_gexp(T, Dk2, kdim, Dk2, kx, nt2 * 8 + gid);
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int mt = mg2 + 2 * i;
+            if (mt < mtn2) {
+              const int a2 = mt * 8 + gid;
+              double av = 0.0;
+              if (a2 < Db2 && kap < kdim) {
+                const cplx bb = Bc[a * ldB + sl * Db2 + a2];
+                av = (kx & 1) ? -bb.y : bb.x;
+              }
+              ic_dmma(acc[i][0], acc[i][1], av, bv);
+            }
+          }
+        }
+      }
+      __syncthreads();  // stage buf and T are rewritten by the next chunk
+    }
+    // env <- E (interleaved, padded rows; entries beyond Db2 x Dk2 zero)
+    for (int e = threadIdx.x; e < MX * ldE; e += IC_THREADS) envd[e] = 0.0;
+    __syncthreads();
+    if (nt2 < ntn2) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int mt = mg2 + 2 * i;
+        const int row = mt * 8 + gid, col = (nt2 * 8 + 2 * tig) >> 1;
+        if (mt < mtn2 && row < Db2 && col < Dk2) {
+          envd[row * ldE + 2 * col] = acc[i][0];
+          envd[row * ldE + 2 * col + 1] = acc[i][1];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[inst] = mk(envd[0], envd[1]);
+}
+
+size_t tt_inner_chunk_smem() {
+  constexpr int MX = 32;
+  return sizeof(double) * MX * (2 * MX + 4) + sizeof(cplx) * ((size_t)MX * IC_SC * MX + 2 * 2 * (size_t)MX * IC_SC * MX);
 }
 
 // ------------------------------------------------------- tt_evaluate_many
@@ -560,7 +722,16 @@ extern "C" int ttp_tt_inner(const ttp_tt_batch* bra, const ttp_tt_batch* ket, do
   int dev = 0, lim = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (smem_staged <= (size_t)lim) {
+  static const bool dmma = [] {
+    const char* e = getenv("TTP_INNER");
+    return !(e && strcmp(e, "scalar") == 0);
+  }();
+  if (dmma && maxb <= 32 && maxk <= 32 && tt_inner_chunk_smem() <= (size_t)lim) {
+    TTP_CUDA_CHECK(ensure_max_smem((const void*)tt_inner_chunk_kernel));
+    LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);
+    tt_inner_chunk_kernel<<<bra->n_inst, IC_THREADS, tt_inner_chunk_smem(), (cudaStream_t)stream>>>(
+        b, k, reinterpret_cast<cplx*>(d_out));
+  } else if (smem_staged <= (size_t)lim) {
     TTP_CUDA_CHECK(ensure_max_smem((const void*)tt_inner_staged_kernel));
     LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);
     tt_inner_staged_kernel<<<bra->n_inst, INNER_THREADS, smem_staged, (cudaStream_t)stream>>>(
