@@ -18,7 +18,7 @@
 
 #include "oracle_eval.cuh"
 
-constexpr int FF_MAXI = 16;  // largest inner coordinate set handled (d <= 32)
+constexpr int FF_MAXI = 10;  // largest inner coordinate set handled (d <= 20)
 
 struct FiberSplit {
   // coordinate positions owned by the row / column of the block
