@@ -108,6 +108,7 @@ __device__ __forceinline__ Cand warp_cand(Cand a) {
 
 struct CC {
   int m, r, C, crank, row0, nrows, ldw;
+  int ns_global;   // the row slices live in global memory (readable by every CTA)
   cplx* Ws;        // local slice, column-major, ld ldw
   cplx* Qg;        // global Q of this instance, column-major, ld m, logical columns
   cplx* aug;       // r x 2r
@@ -1577,7 +1578,18 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
   for (long long it = 0;; ++it) {
     a = warp_cand(a);
     __syncwarp();
-    warp_publish(c, par, a);
+    if (c.ns_global) {
+      // global-slice mode: the winner's row is read straight from its
+      // owner's slice after the barrier, so only the record is published
+      WCand* slot = &c.wrec[par * CW + warp];
+      if (lane == 0) {
+        slot->v = a.v;
+        slot->key = a.key;
+        slot->row = a.row >= 0 ? lo + a.row : -1;
+      }
+    } else {
+      warp_publish(c, par, a);
+    }
     SP(spt, 8);
     cl.sync();
     SP(spt, 9);
@@ -1586,7 +1598,13 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
       const int i = W.w.row;
       const int j = (int)(W.w.key - (long long)i * r);
       cplx x0, x1;
-      winner_row(cl, c, par, W, x0, x1);
+      if (c.ns_global) {
+        const cplx* rowp = c.Ws + (long long)(W.rank - c.crank) * c.ldw * r + (i - W.rank * c.ldw);
+        x0 = (lane < r) ? rowp[(long long)lane * c.ldw] : mk(0.0, 0.0);
+        x1 = (lane + 32 < r) ? rowp[(long long)(lane + 32) * c.ldw] : mk(0.0, 0.0);
+      } else {
+        winner_row(cl, c, par, W, x0, x1);
+      }
       const cplx pivot = lane_entry(x0, x1, j);
       // candidates are ranked by |b|^2; the stopping test uses |b| (hypot, as numpy abs)
       const int done = (cabsh(pivot) <= 1.0 + slack) ? 1 : 0;
@@ -1732,6 +1750,7 @@ __global__ void __launch_bounds__(CT, 1) cluster_bond_kernel(ClusterJob J) {
   c.Qg = J.Qg + inst * J.q_stride;
   carve(smem_raw, ms, job.r, &c, J.Wg != nullptr, J.big != 0);
   if (J.Wg) c.Ws = J.Wg + inst * J.wg_stride + (long long)c.crank * ms * job.r;
+  c.ns_global = J.Wg != nullptr;
   if (J.big) {
     c.vn1 = job.dwork + inst * job.dw_stride + (long long)c.crank * 2 * ms;
     c.vn2 = c.vn1 + ms;
