@@ -67,6 +67,8 @@ constexpr int CT = CLUSTER_THREADS;
 constexpr int CW = CT / 32;
 constexpr int RMAX = 64;
 constexpr int QX_ROWS = 64;  // rows per staged tile of the DMMA Q*X products
+constexpr int LAZY_MAX = 4;  // most deferred swap updates (global-slice mode)
+__constant__ int g_lazy_f = LAZY_MAX;  // flush cadence of the deferred updates (1 = eager)
 __constant__ int g_serpentine = 1;  // dev knob (A/B of the serpentine row order)
 
 struct __align__(16) Rec {
@@ -140,6 +142,8 @@ struct CC {
   int* ibc;        // 8
   double* dbc;     // 8
   cplx* cbc;       // 8
+  cplx* pend;      // [LAZY_MAX][r] deferred swap updates w_s (global-slice mode), or nullptr
+  int* pendj;      // [LAZY_MAX] their pivot columns j_s
 };
 
 __device__ __forceinline__ cplx& Wl(const CC& c, int l, int t) { return c.Ws[(long long)t * c.ldw + l]; }
@@ -291,6 +295,8 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
   t.ibc = (int*)take(sizeof(int) * 16);
   t.dbc = (double*)take(sizeof(double) * 8);
   t.cbc = (cplx*)take(sizeof(cplx) * 8);
+  t.pend = global_slice ? (cplx*)take(sizeof(cplx) * LAZY_MAX * r) : nullptr;
+  t.pendj = global_slice ? (int*)take(sizeof(int) * LAZY_MAX) : nullptr;
   if (c) {
     c->Ws = t.Ws; c->aug = t.aug; c->selb = t.selb; c->vec = t.vec; c->vec2 = t.vec2;
     c->tau = t.tau; c->betas = t.betas; c->cn1 = t.cn1; c->cn2 = t.cn2; c->colmap = t.colmap;
@@ -299,6 +305,7 @@ __host__ __device__ size_t carve(unsigned char* base, int ldw, int r, CC* c, boo
     c->wrec = t.wrec; c->wrow = t.wrow;
     c->wrec2 = t.wrec2; c->rpos2 = t.rpos2; c->sp = t.sp; c->qtile = t.qtile;
     c->wss = t.wss; c->ibc = t.ibc; c->dbc = t.dbc; c->cbc = t.cbc;
+    c->pend = t.pend; c->pendj = t.pendj;
   }
   return off;
 }
@@ -1567,10 +1574,96 @@ __device__ void start_pair_s(cg::cluster_group& cl, CC& c, int& par) {
 }
 
 // ---------------------------------------------------------- phase D
-__device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, double slack, long long limit) {
+// Split cluster barrier (all threads of every CTA): arrive has release and
+// wait acquire semantics, so memory reads before a peer's arrive happen
+// before writes after my wait.
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// One row pass of the swaps over my rows with NP updates still to apply:
+// entry (l, t) of the current B is
+//   B_W[l, t] + sum_{s < NP} c_s(l) w_s[t],   c_s(l) = B_{s-1}[l, j_s],
+// with B_W the slice as stored and c_s(l) accumulated by the same fma chain
+// the eager updates would have run, so every value (and the argmax) is
+// bitwise the eager one.  flush: write the current B back (B_W := B).
+// Returns my best |B|^2 candidate.
+template <int NP>
+__device__ __forceinline__ Cand swap_pass(const CC& c, const cplx* pw, const int* pj, bool flush, bool rev) {
   const int r = c.r, lo = c.row0, nl = c.nrows;
+  // running best as (|v|^2, 32-bit row-major key): fewer live registers
+  // than a Cand in the hottest loop; the row follows from the key
+  double bv = -1.0;
+  int bk = INT_MAX;
+  FOR_MY_ROWS(l, nl, rev) {
+    cplx* p = c.Ws + l;
+    const long long ld = c.ldw;
+    cplx cs[NP];
+#pragma unroll
+    for (int s = 0; s < NP; ++s) cs[s] = p[pj[s] * ld];
+#pragma unroll
+    for (int s = 1; s < NP; ++s)
+#pragma unroll
+      for (int u = 0; u < s; ++u) cs[s] = cfma(cs[u], pw[u * r + pj[s]], cs[s]);
+    const int rk = (lo + l) * r;
+    int t = 0;
+    // the hottest loop: 16 loads in flight (8 with three or more pending
+    // updates, whose coefficients take the registers)
+    constexpr int KS = NP <= 2 ? 2 * KB : KB;
+    for (; t + KS <= r; t += KS) {
+      cplx x[KS];
+#pragma unroll
+      for (int q = 0; q < KS; ++q) x[q] = p[(t + q) * ld];
+#pragma unroll
+      for (int q = 0; q < KS; ++q) {
+        cplx v = x[q];
+#pragma unroll
+        for (int s = 0; s < NP; ++s) v = cfma(cs[s], pw[s * r + t + q], v);
+        if (flush) p[(t + q) * ld] = v;
+        const double v2 = cabs2(v);
+        if (v2 > bv || (v2 == bv && rk + t + q < bk)) {
+          bv = v2;
+          bk = rk + t + q;
+        }
+      }
+    }
+    for (; t < r; ++t) {
+      cplx v = p[t * ld];
+#pragma unroll
+      for (int s = 0; s < NP; ++s) v = cfma(cs[s], pw[s * r + t], v);
+      if (flush) p[t * ld] = v;
+      const double v2 = cabs2(v);
+      if (v2 > bv || (v2 == bv && rk + t < bk)) {
+        bv = v2;
+        bk = rk + t;
+      }
+    }
+  }
+  Cand a{-1.0, LLONG_MAX, -1};
+  if (bk != INT_MAX) a = Cand{bv, (long long)bk, bk / r - lo};
+  return a;
+}
+
+// _swap_to_dominance (cross.py:122-139).  In global-slice mode the rank-1
+// updates are deferred: up to g_lazy_f of them are folded into read-only row
+// passes, and every g_lazy_f-th pass writes the slice back, which halves the
+// slice traffic of most passes (the passes are HBM bound at full occupancy).
+__device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, double slack, long long limit) {
+  const int r = c.r, lo = c.row0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  cplx* S = c.vec2;  // [0, r): B[i, :] before the update; [r, 2r): w
+  cplx* S = c.vec2;  // [0, r): B[i, :] before the update; [r, 2r): w (eager mode)
+  const bool lazy = c.pend != nullptr;
+  cplx* pw = lazy ? c.pend : S + r;      // pending w_s, s < np
+  int* pj = lazy ? c.pendj : c.ibc + 8;  // pending j_s
+  const int F = lazy ? max(1, min(LAZY_MAX, g_lazy_f)) : 1;
+  int np = 0;  // updates not yet written to the slice
+  // global-slice mode: peers read winner rows straight from my slice, so no
+  // CTA may rewrite its slice (form_B, a flushing pass) while a peer can
+  // still be reading the previous winner row from it
+  if (c.ns_global) cl.sync();
   invert_rows(c, c.sel);
   Cand a = form_B(c);
   int status = TTP_ERR_MAXVOL_ITER;
@@ -1602,6 +1695,12 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
         const cplx* rowp = c.Ws + (long long)(W.rank - c.crank) * c.ldw * r + (i - W.rank * c.ldw);
         x0 = (lane < r) ? rowp[(long long)lane * c.ldw] : mk(0.0, 0.0);
         x1 = (lane + 32 < r) ? rowp[(long long)(lane + 32) * c.ldw] : mk(0.0, 0.0);
+        // the pending updates, in order (the owner's row pass ran the same chain)
+        for (int s = 0; s < np; ++s) {
+          const cplx cv = lane_entry(x0, x1, pj[s]);
+          if (lane < r) x0 = cfma(cv, pw[s * r + lane], x0);
+          if (lane + 32 < r) x1 = cfma(cv, pw[s * r + lane + 32], x1);
+        }
       } else {
         winner_row(cl, c, par, W, x0, x1);
       }
@@ -1610,14 +1709,16 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
       const int done = (cabsh(pivot) <= 1.0 + slack) ? 1 : 0;
       if (!done && it < limit) {
         // w[t] = (B[sel[j], t] - B[i, t]) / pivot: one fma per entry in the update
+        cplx* w = pw + np * r;
         if (lane < r) {
           S[lane] = x0;
-          S[r + lane] = cdiv(csub(c.selb[j * r + lane], x0), pivot);
+          w[lane] = cdiv(csub(c.selb[j * r + lane], x0), pivot);
         }
         if (lane + 32 < r) {
           S[lane + 32] = x1;
-          S[r + lane + 32] = cdiv(csub(c.selb[j * r + lane + 32], x1), pivot);
+          w[lane + 32] = cdiv(csub(c.selb[j * r + lane + 32], x1), pivot);
         }
+        if (lane == 0) pj[np] = j;
       }
       if (lane == 0) {
         c.ibc[4] = i;
@@ -1635,7 +1736,14 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
       break;
     }
     par ^= 1;
-    const cplx* w = S + r;
+    const int nq = np + 1;
+    const bool flush = nq >= F;
+    const bool refresh = (it + 1) % 64 == 0;
+    // this iteration rewrites the slice: every CTA must be done reading the
+    // winner row first (the barrier latency overlaps the B[sel, :] update)
+    const bool fence = c.ns_global && (flush || refresh);
+    if (fence) cluster_arrive();
+    const cplx* w = pw + np * r;
     // replicated B[sel, :]: rank-1 update of every row, row j <- updated B[i, :]
     for (int q = warp; q < r; q += CW) {
       const cplx bqj = (q == j) ? S[j] : c.selb[q * r + j];
@@ -1648,38 +1756,22 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
       if (lane + 32 < r) c.selb[q * r + lane + 32] = y1;
     }
     if (threadIdx.x == 0) c.sel[j] = i;
+    if (fence) cluster_wait();
     SP(spt, 12);
-    a = Cand{-1.0, LLONG_MAX, -1};
-    FOR_MY_ROWS(l, nl, g_serpentine && ((it & 1) == 0)) {
-      const cplx blj = Wl(c, l, j);
-      cplx* p = c.Ws + l;
-      const long long ld = c.ldw;
-      int t = 0;
-      constexpr int KS = 2 * KB;  // the swap pass is the hottest loop: 16 loads in flight
-      for (; t + KS <= r; t += KS) {
-        cplx x[KS];
-#pragma unroll
-        for (int q = 0; q < KS; ++q) x[q] = p[(t + q) * ld];
-#pragma unroll
-        for (int q = 0; q < KS; ++q) {
-          const cplx v = cfma(blj, w[t + q], x[q]);
-          p[(t + q) * ld] = v;
-          const Cand b{cabs2(v), (long long)(lo + l) * r + t + q, l};
-          if (cand_better(b, a)) a = b;
-        }
-      }
-      for (; t < r; ++t) {
-        const cplx v = cfma(blj, w[t], p[t * ld]);
-        p[t * ld] = v;
-        const Cand b{cabs2(v), (long long)(lo + l) * r + t, l};
-        if (cand_better(b, a)) a = b;
-      }
+    const bool rev = g_serpentine && ((it & 1) == 0);
+    switch (nq) {
+      case 1: a = swap_pass<1>(c, pw, pj, flush, rev); break;
+      case 2: a = swap_pass<2>(c, pw, pj, flush, rev); break;
+      case 3: a = swap_pass<3>(c, pw, pj, flush, rev); break;
+      default: a = swap_pass<4>(c, pw, pj, flush, rev); break;
     }
+    np = flush ? 0 : nq;
     SP(spt, 13);
-    if ((it + 1) % 64 == 0) {
+    if (refresh) {
       __syncthreads();
       invert_rows(c, c.sel);
       a = form_B(c);
+      np = 0;
     }
   }
   par ^= 1;
@@ -1982,8 +2074,24 @@ static bool fused_starts_enabled() {
   return on;
 }
 
+// TTP_LAZY=F (1..LAZY_MAX): flush cadence of the deferred swap updates in
+// global-slice mode (1 = the eager update of every row pass); A/B knob.
+static cudaError_t apply_lazy_knob() {
+  static const cudaError_t st = [] {
+    const char* e = getenv("TTP_LAZY");
+    if (!e) return cudaSuccess;
+    const int f = std::max(1, std::min(LAZY_MAX, atoi(e)));
+    return cudaMemcpyToSymbol(g_lazy_f, &f, sizeof(int));
+  }();
+  return st;
+}
+
 cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream_t s) {
   ClusterJob job = job_in;
+  {
+    const cudaError_t e = apply_lazy_knob();
+    if (e != cudaSuccess) return e;
+  }
   resolve_big(job);
   job.q_wy = q_wy_enabled() ? 1 : 0;
   job.fused_starts = fused_starts_enabled() ? 1 : 0;
