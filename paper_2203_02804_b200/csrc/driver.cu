@@ -227,6 +227,21 @@ int l2_cluster_size() {
 }
 bool force_v0() { return bond_path_mode() == 1; }
 
+// Global-slice clusters: the 256-thread, two-CTAs-per-SM instantiation
+// (ck_tp) for throughput batches, the 512-thread one (ck_lat) when a few
+// instances leave SMs idle anyway.  TTP_CK=lat|tp forces one (A/B knob).
+static int tp_knob() {
+  static const int forced = [] {
+    const char* e = getenv("TTP_CK");
+    if (e && std::strcmp(e, "lat") == 0) return 0;
+    if (e && std::strcmp(e, "tp") == 0) return 1;
+    return -1;
+  }();
+  return forced;
+}
+bool tp_forced() { return tp_knob() == 1; }
+bool use_tp_kernel(int n) { return tp_knob() >= 0 ? tp_knob() == 1 : n > 16; }
+
 size_t smem_optin_limit() {
   static size_t lim = [] {
     int dev = 0, v = 0;
@@ -250,7 +265,7 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
   const long long block_bytes = (long long)bj.m * bj.r * (long long)sizeof(cplx);
   // small batches of blocks too large for a shared-memory cluster (r = 64,
   // cfg5) also take the global-slice kernel, with more CTAs per instance
-  const bool smem_fits = !force_v0() && pick_cluster_size(bj.m, bj.r, smem_optin_limit()) > 0;
+  const bool smem_fits = !force_v0() && ck_lat::pick_cluster_size(bj.m, bj.r, smem_optin_limit()) > 0;
   const bool auto_l2 = bond_path_mode() == 0 && block_bytes >= (1LL << 20) && (n > 16 || !smem_fits);
   if (bond_path_mode() == 3 || auto_l2) {
     ClusterJob cj{};
@@ -268,12 +283,19 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
     cj.Wg = w.W;
     cj.Sg = w.B;
     cj.wg_stride = w.mat_stride;
-    if (max_active_clusters(cj) > 0) {
-      TTP_CUDA_CHECK(launch_cluster_bond(cj, n, s));
+    // throughput batches take the two-CTAs-per-SM instantiation when its
+    // carve fits twice per SM (r <= 32); r = 64 stays on 512-thread CTAs
+    if (use_tp_kernel(n) && (tp_forced() || ck_tp::max_active_clusters(cj) > ck_lat::max_active_clusters(cj))) {
+      if (ck_tp::max_active_clusters(cj) > 0) {
+        TTP_CUDA_CHECK(ck_tp::launch_cluster_bond(cj, n, s));
+        return TTP_OK;
+      }
+    } else if (ck_lat::max_active_clusters(cj) > 0) {
+      TTP_CUDA_CHECK(ck_lat::launch_cluster_bond(cj, n, s));
       return TTP_OK;
     }
   }
-  const int C = force_v0() ? 0 : pick_cluster_size(bj.m, bj.r, smem_optin_limit());
+  const int C = force_v0() ? 0 : ck_lat::pick_cluster_size(bj.m, bj.r, smem_optin_limit());
   if (C > 0) {
     ClusterJob cj{};
     cj.b = bj;
@@ -284,10 +306,10 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
     cj.fiber = f;
     cj.Qg = w.A;
     cj.q_stride = w.mat_stride;
-    const int act = max_active_clusters(cj);
+    const int act = ck_lat::max_active_clusters(cj);
     const bool use = act > 0 && (bond_path_mode() == 2 || n <= 2 * act);
     if (use) {
-      TTP_CUDA_CHECK(launch_cluster_bond(cj, n, s));
+      TTP_CUDA_CHECK(ck_lat::launch_cluster_bond(cj, n, s));
       return TTP_OK;
     }
   }
@@ -624,7 +646,7 @@ extern "C" int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const doubl
   bj.sel_stride = cols;
   bj.write_mode = 0;
   TTP_CUDA_CHECK(cudaMemsetAsync(bj.status, 0, sizeof(int) * n_mat, s));
-  const int C = force_v0() ? 0 : pick_cluster_size((int)rows, cols, smem_optin_limit());
+  const int C = force_v0() ? 0 : ck_lat::pick_cluster_size((int)rows, cols, smem_optin_limit());
   ClusterJob cj{};
   cj.b = bj;
   cj.cl = C;
@@ -633,8 +655,8 @@ extern "C" int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const doubl
   cj.src_stride = mr;
   cj.Qg = bj.A;
   cj.q_stride = mr;
-  if (C > 0 && max_active_clusters(cj) > 0) {
-    TTP_CUDA_CHECK(launch_cluster_bond(cj, n_mat, s));
+  if (C > 0 && ck_lat::max_active_clusters(cj) > 0) {
+    TTP_CUDA_CHECK(ck_lat::launch_cluster_bond(cj, n_mat, s));
   } else {
     dim3 grid((unsigned)((mr + 255) / 256), (unsigned)n_mat);
     {
@@ -711,4 +733,20 @@ extern "C" int ttp_price_tt_batch(const ttp_price_problem* prob, ttp_cross_out* 
     h_imag[i] = ok ? prob->h_prefactor[i] * raw[2 * i + 1] : NAN;
   }
   return TTP_OK;
+}
+
+// Phase clocks of whichever cluster instantiation ran since the last enable
+// (dev tool tools/phase_timing.py).
+extern "C" int ttp_debug_phase_clocks(int enable, int64_t* out, int32_t n) {
+  int64_t a[32] = {}, b[32] = {};
+  int st = ck_tp::debug_phase_clocks(0, a, 32);
+  if (st == TTP_OK) st = ck_lat::debug_phase_clocks(0, b, 32);
+  if (st != TTP_OK) return st;
+  if (out && n > 0) {
+    const int64_t* src = (a[8] != 0 || a[1] != 0) ? a : b;
+    for (int i = 0; i < n && i < 32; ++i) out[i] = src[i];
+  }
+  st = ck_tp::debug_phase_clocks(enable, nullptr, 0);
+  if (st == TTP_OK) st = ck_lat::debug_phase_clocks(enable, nullptr, 0);
+  return st;
 }

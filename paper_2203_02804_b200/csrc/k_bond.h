@@ -47,7 +47,10 @@ cudaError_t launch_bond(const BondJob& job, int n_inst, cudaStream_t s);
 
 // Cluster variant (k_cluster.cu): one thread-block cluster per instance, the
 // block resident in distributed shared memory.
-#define CLUSTER_THREADS 512
+// Two instantiations (k_cluster_impl.cuh): ck_lat (512 threads, one CTA
+// per SM; latency: single options, shared-memory clusters) and ck_tp (256
+// threads, two CTAs per SM; throughput batches of global-slice clusters,
+// where two instances per SM hide each other's barrier and latency stalls).
 
 struct ClusterJob {
   BondJob b;              // shared fields (A/W/B/iwork/dwork unused)
@@ -56,7 +59,7 @@ struct ClusterJob {
   int fiber_fast;         // src_mode 0: separable evaluation allowed (fiber_fast.cuh)
   int q_wy;               // form Q in compact-WY form (else zung2r rounds)
   int fused_starts;       // both dominant-row starts in one read-only pass sequence
-  int big;                // per-row arrays and B[sel,:] in global memory (set by the launcher)
+  int big;                // bit 0: per-row arrays, bit 1: B[sel,:] in global memory (set by the launcher)
   cplx* Sg;               // global-slice mode: B buffer (holds B[sel,:] in big mode), stride wg_stride
   int debug_start;        // dev aid (TTP_DEBUG_START=1|2): return start set 1 or 2
   OracleDev oracle;
@@ -73,7 +76,11 @@ struct ClusterJob {
   long long wg_stride;
 };
 
-size_t cluster_smem_bytes(int m, int r, int C, bool global_slice = false, bool big = false);
-int pick_cluster_size(int m, int r, size_t smem_limit);  // 0 if no cluster fits
-int max_active_clusters(const ClusterJob& job);
-cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s);
+#define TTP_CLUSTER_API                                                                     \
+  size_t cluster_smem_bytes(int m, int r, int C, bool global_slice = false, int big = 0);   \
+  int pick_cluster_size(int m, int r, size_t smem_limit); /* 0 if no cluster fits */        \
+  int max_active_clusters(const ClusterJob& job);                                           \
+  cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s);       \
+  int debug_phase_clocks(int enable, int64_t* out, int32_t n);
+namespace ck_lat { TTP_CLUSTER_API }
+namespace ck_tp { TTP_CLUSTER_API }
