@@ -253,6 +253,40 @@ __device__ __forceinline__ cplx col_dotc(const CC& c, int ci, int cj, int l0, in
   return acc;
 }
 
+// col_dotc for n <= G columns cols[0..n) against column ci, reading column
+// ci once for all of them (same per-lane accumulation order as col_dotc)
+template <int G>
+__device__ __forceinline__ void col_dotc_group(const CC& c, int ci, const int* cols, int n, int l0, int nl,
+                                               cplx* acc) {
+  const cplx* a = c.Ws + (long long)ci * c.ldw;
+  const cplx* b[G];
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    b[k] = c.Ws + (long long)cols[min(k, n - 1)] * c.ldw;
+    acc[k] = mk(0.0, 0.0);
+  }
+  int l = l0;
+  constexpr int RB = (12 / (G + 1)) > 1 ? 12 / (G + 1) : 1;  // ~12 loads in flight
+  for (; l + 32 * (RB - 1) < nl; l += 32 * RB) {
+    cplx x[RB], y[RB][G];
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      x[u] = a[l + 32 * u];
+#pragma unroll
+      for (int k = 0; k < G; ++k) y[u][k] = b[k][l + 32 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < RB; ++u)
+#pragma unroll
+      for (int k = 0; k < G; ++k) acc[k] = cfmac(x[u], y[u][k], acc[k]);
+  }
+  for (; l < nl; l += 32) {
+    const cplx x = a[l];
+#pragma unroll
+    for (int k = 0; k < G; ++k) acc[k] = cfmac(x, b[k][l], acc[k]);
+  }
+}
+
 // big: (global-slice mode, blocks whose normal carve exceeds shared memory,
 // e.g. r = 64) the per-row arrays vn1/vn2/rpos/rpos2 and B[sel,:] live in
 // global memory (the instance's dwork/iwork and B buffers) instead.
@@ -727,9 +761,13 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
     const int lstart = max(0, i + 1 - lo);  // first local row with global index > i
     const int ntr = r - i - 1;
     Rec* me = &c.rec[par];
-    // partials: task 0 = Ssq of x, task q>=1 = conj(x) . column (i+q)
-    for (int q = warp; q <= ntr; q += CW) {
-      if (q == 0) {
+    // partials: item 0 = Ssq of x, item g >= 1 = conj(x) . columns i+q for
+    // the PG tasks q of group g (column x read once per group; PG sized so
+    // that every item gets its own warp)
+    const int PG = min(8, max(1, (ntr + CW - 2) / (CW - 1)));
+    const int ngrp = (ntr + PG - 1) / PG;
+    for (int it = warp; it <= ngrp; it += CW) {
+      if (it == 0) {
         const int f0 = lstart + lane;
         Ssq s = ssq_of(&c.Ws[(long long)ci * c.ldw + f0], 32, nl > f0 ? (nl - f0 + 31) / 32 : 0);
         s = warp_ssq(s);
@@ -738,13 +776,27 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
           me->data[1] = own_i ? Wl(c, li, ci) : mk(0.0, 0.0);
         }
       } else {
-        const int cj = c.colmap[i + q];
-        cplx acc = mk(0.0, 0.0);
-        acc = col_dotc(c, ci, cj, lstart + lane, nl);
-        acc = warp_sum(acc);
-        if (lane == 0) {
-          me->data[1 + q] = acc;
-          me->data[1 + r + q] = own_i ? Wl(c, li, cj) : mk(0.0, 0.0);
+        const int q0 = 1 + (it - 1) * PG;
+        const int n = min(PG, ntr - q0 + 1);
+        cplx acc[8];
+        const int* cols = c.colmap + i + q0;
+        switch (PG) {
+          case 1: col_dotc_group<1>(c, ci, cols, n, lstart + lane, nl, acc); break;
+          case 2: col_dotc_group<2>(c, ci, cols, n, lstart + lane, nl, acc); break;
+          case 3: col_dotc_group<3>(c, ci, cols, n, lstart + lane, nl, acc); break;
+          case 4: col_dotc_group<4>(c, ci, cols, n, lstart + lane, nl, acc); break;
+          case 5: col_dotc_group<5>(c, ci, cols, n, lstart + lane, nl, acc); break;
+          default: col_dotc_group<8>(c, ci, cols, n, lstart + lane, nl, acc); break;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k < n) {
+            const cplx sum = warp_sum(acc[k]);
+            if (lane == 0) {
+              me->data[q0 + k + 1] = sum;
+              me->data[1 + r + q0 + k] = own_i ? Wl(c, li, c.colmap[i + q0 + k]) : mk(0.0, 0.0);
+            }
+          }
         }
       }
     }
