@@ -991,7 +991,7 @@ __device__ void qx_dmma(const CC& c, const cplx* X, int ldx, Sink sink) {
   const int ntn = (2 * r + 7) / 8;
   const int nt = warp & 7, mgrp = warp >> 3;
   constexpr int MG = CW / 8;  // warp groups over m-tiles
-  const bool active = nt < ntn;
+  const bool active = nt < ntn && warp < 8 * MG;  // CW need not be a multiple of 8
   double breg[16];
 #pragma unroll
   for (int ks = 0; ks < 16; ++ks) {

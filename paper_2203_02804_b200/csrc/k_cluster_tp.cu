@@ -5,7 +5,13 @@
 // rest of the unified L1 to the row passes (measured +4% options/s on cfg4
 // against one 512-thread CTA per SM, profiles/r01/ab_cta_shape.log).
 #define CK_NS ck_tp
-#define CLUSTER_THREADS 256
+#ifndef TP_THREADS
+#define TP_THREADS 256
+#endif
+#ifndef TP_QX_ROWS
+#define TP_QX_ROWS 16
+#endif
+#define CLUSTER_THREADS TP_THREADS
 #define CLUSTER_MIN_BLOCKS 2
-#define QX_ROWS_DEF 16
+#define QX_ROWS_DEF TP_QX_ROWS
 #include "k_cluster_impl.cuh"
