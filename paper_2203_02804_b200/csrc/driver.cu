@@ -220,8 +220,11 @@ int bond_path_mode() {
 int l2_cluster_size() {
   static const int v = [] {
     const char* e = getenv("TTP_BOND_PATH");
-    if (e && std::strncmp(e, "l2:", 3) == 0) return std::max(1, atoi(e + 3));
-    return 8;
+    // powers of two only (the row split assumes it; 3-CTA clusters fault)
+    int c = (e && std::strncmp(e, "l2:", 3) == 0) ? std::max(1, atoi(e + 3)) : 8;
+    int p = 1;
+    while (p * 2 <= std::min(c, 16)) p *= 2;
+    return p;
   }();
   return v;
 }
