@@ -484,6 +484,7 @@ size_t conv_site_smem(int ra, int rb, int threads) {
 constexpr int CD_ROWS = 64;
 constexpr int CD_THREADS = 256;
 constexpr int CD_MT = 4;  // m-tiles (8 rows) per warp
+static_assert(CD_THREADS % CD_ROWS == 0, "gather: whole threads per row");
 
 __host__ __device__ inline int cd_kp(int ra) { return ((2 * ra + 3) & ~3) + 4; }  // padded row stride (doubles)
 
@@ -493,7 +494,9 @@ __device__ __forceinline__ double cd_bfrag(const cplx* G, int ra, int rb, int k0
   const int a = k >> 1, p = k & 1, c = ncol >> 1, q = ncol & 1;
   if (a >= ra || c >= rb) return 0.0;
   const cplx g = G[a * rb + c];
-  return (p == q) ? g.x : (q ? g.y : -g.y);
+  // -Im by a sign-bit flip (integer pipe; the FP64 pipe feeds the DMMA)
+  const double im = (q ? g.y : __longlong_as_double(__double_as_longlong(g.y) ^ (long long)0x8000000000000000ULL));
+  return (p == q) ? g.x : im;
 }
 
 // KS > 0: all KS x NT B' fragments of the warp live in registers (formed
@@ -519,18 +522,21 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
   const cplx* vin = Vin + inst * vstride;
   cplx* vout = Vout + inst * vstride;
   const int ntile = (g1 - g0 + CD_ROWS - 1) / CD_ROWS;
+  // gather of one tile: CD_THREADS / CD_ROWS threads per row, each loading
+  // the row's sample index once and copying every TPR-th 16-byte chunk
   auto issue = [&](int tile, int buf) {
+    constexpr int TPR = CD_THREADS / CD_ROWS;
     double* st = buf ? stage1 : stage0;
     int* rj = rowj + buf * CD_ROWS;
     const int t0 = g0 + tile * CD_ROWS;
-    const int chunks = ra;  // 16-byte chunks per row
-    for (int e = threadIdx.x; e < CD_ROWS * chunks; e += CD_THREADS) {
-      const int row = e / chunks, ch = e - row * chunks;
-      const int t = min(t0 + row, g1 - 1);
-      const int j = perm[t];
-      if (ch == 0) rj[row] = (t0 + row < g1) ? j : -1;
-      cp_async16(st + row * KP + 2 * ch, vin + (long long)j * ra + ch);
-    }
+    const int row = threadIdx.x / TPR, cg = threadIdx.x - row * TPR;
+    const int t = min(t0 + row, g1 - 1);
+    const int j = perm[t];
+    if (cg == 0) rj[row] = (t0 + row < g1) ? j : -1;
+    const cplx* srow = vin + (long long)j * ra;
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(st + row * KP);
+    for (int ch = cg; ch < ra; ch += TPR)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * ch), "l"(srow + ch));
     cp_async_commit();
   };
   issue(0, 0);  // first gather overlaps the slice load below
