@@ -524,14 +524,15 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
   const int ntile = (g1 - g0 + CD_ROWS - 1) / CD_ROWS;
   // gather of one tile: CD_THREADS / CD_ROWS threads per row, each loading
   // the row's sample index once and copying every TPR-th 16-byte chunk
-  auto issue = [&](int tile, int buf) {
-    constexpr int TPR = CD_THREADS / CD_ROWS;
+  // (the sample index of a row is loaded one tile ahead: sample_j)
+  constexpr int TPR = CD_THREADS / CD_ROWS;
+  const int grow = threadIdx.x / TPR, gcg = threadIdx.x - grow * TPR;
+  auto sample_j = [&](int tile) { return tile < ntile ? perm[min(g0 + tile * CD_ROWS + grow, g1 - 1)] : 0; };
+  auto issue = [&](int tile, int buf, int j) {
     double* st = buf ? stage1 : stage0;
     int* rj = rowj + buf * CD_ROWS;
     const int t0 = g0 + tile * CD_ROWS;
-    const int row = threadIdx.x / TPR, cg = threadIdx.x - row * TPR;
-    const int t = min(t0 + row, g1 - 1);
-    const int j = perm[t];
+    const int row = grow, cg = gcg;
     if (cg == 0) rj[row] = (t0 + row < g1) ? j : -1;
     const cplx* srow = vin + (long long)j * ra;
     const unsigned dst = (unsigned)__cvta_generic_to_shared(st + row * KP);
@@ -539,7 +540,8 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * ch), "l"(srow + ch));
     cp_async_commit();
   };
-  issue(0, 0);  // first gather overlaps the slice load below
+  issue(0, 0, sample_j(0));  // first gather overlaps the slice load below
+  int jnext = sample_j(1);
   const cplx* src = cores + inst * stride + offk;
   for (int e = threadIdx.x; e < ra * rb; e += CD_THREADS) {
     const int a = e / rb, c = e - a * rb;
@@ -566,7 +568,8 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
   for (int tile = 0; tile < ntile; ++tile) {
     const int buf = tile & 1;
     if (tile + 1 < ntile) {
-      issue(tile + 1, buf ^ 1);
+      issue(tile + 1, buf ^ 1, jnext);
+      jnext = sample_j(tile + 2);
       cp_async_wait_all_but_one();
     } else {
       cp_async_wait_all();
