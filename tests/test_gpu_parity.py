@@ -400,6 +400,70 @@ def test_full_size_cfg4_batch_properties():
         assert abs(P.tt_inner(tt, tt) - O.tt_inner(tt.cores, tt.cores)) <= 1e-12 * abs(O.tt_inner(tt.cores, tt.cores))
 
 
+_CK_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_2203_02804_b200 as P
+from paper_2203_02804_b200 import configs
+spec = configs.CONFIGS[4]
+shape = (spec.grid.points_per_axis,) * spec.d
+cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+ms = [configs.make_model(4, i) for i in range(17)]
+b = P.tt_cross_batch([P.PhiGridOracle(m, spec.grid) for m in ms], shape, cfg, with_reports=False)
+assert all(s == 0 for s in b.status)
+tr = b.trains.to_trains()
+np.savez(sys.argv[1], *[c for i in (0, 8, 16) for c in tr[i].cores])
+"""
+
+
+def test_throughput_and_latency_cluster_kernels_agree(tmp_path):
+    """A cfg4 batch of 17 (global-slice clusters) gives the same cores
+    bitwise from the 256-thread two-CTAs-per-SM instantiation and the
+    512-thread one (TTP_CK forces each in its own process)."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "ck.py"
+    script.write_text(_CK_SCRIPT)
+    out = {}
+    for ck in ("tp", "lat"):
+        env = dict(os.environ, TTP_CK=ck)
+        path = tmp_path / f"{ck}.npz"
+        subprocess.run([sys.executable, str(script), str(path)], check=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+        out[ck] = np.load(path)
+    assert len(out["tp"].files) == len(out["lat"].files) > 0
+    for k in out["tp"].files:
+        np.testing.assert_array_equal(out["tp"][k], out["lat"][k])
+
+
+def test_throughput_kernel_batch_composition_and_properties():
+    """Batches above 16 take the throughput instantiation: an instance's
+    cores do not depend on its batch neighbours or position, repeated runs
+    are bitwise identical, and the interpolation property holds at the
+    final pivots."""
+    spec = configs.CONFIGS[4]
+    models = [configs.make_model(4, i) for i in range(18)]
+    shape = (spec.grid.points_per_axis,) * spec.d
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    a = P.tt_cross_batch([P.PhiGridOracle(m, spec.grid) for m in models], shape, cfg)
+    b = P.tt_cross_batch([P.PhiGridOracle(m, spec.grid) for m in models[1:]], shape, cfg)
+    c = P.tt_cross_batch([P.PhiGridOracle(m, spec.grid) for m in models], shape, cfg)
+    assert all(s == 0 for s in a.status) and all(s == 0 for s in b.status)
+    ta, tb, tc = a.trains.to_trains(), b.trains.to_trains(), c.trains.to_trains()
+    for i in (1, 9, 17):
+        for x, y, z in zip(ta[i].cores, tb[i - 1].cores, tc[i].cores):
+            np.testing.assert_array_equal(x, y)
+            np.testing.assert_array_equal(x, z)
+    for i in (0, 17):
+        rep, tt = a.reports[i], ta[i]
+        oracle = P.PhiGridOracle(models[i], spec.grid)
+        k = spec.d // 2
+        idx = np.array([p + q for p in rep.left_sets[k] for q in rep.right_sets[k]])
+        got, want = P.tt_evaluate_many(tt, idx), oracle(idx)
+        assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))
+
+
 def test_batch_prices_equal_single_prices():
     spec = configs.CONFIGS[3]
     models = [configs.make_model(3, i) for i in range(6)]
