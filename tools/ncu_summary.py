@@ -1,6 +1,6 @@
 """Summarise a round's ncu artefacts into profiles/ (dev tool, runs here).
 
-usage: python tools/ncu_summary.py <prof dir> <round tag>
+usage: python tools/ncu_summary.py <prof dir> <round tag> [--no-traffic]
   * launch list (gpu__time_duration per launch) -> per-kernel totals/shares
   * each .ncu-rep -> key metrics (duration, DRAM bytes, pipe utilisation,
     occupancy, stall reasons) and profiles/ncu_traffic.json (DRAM bytes per
@@ -19,7 +19,8 @@ dst = os.path.join("profiles", tag)
 os.makedirs(dst, exist_ok=True)
 
 # ---- launch list
-rows = list(csv.reader(open(os.path.join(src, "launches.csv"))))
+lpath = os.path.join(src, "launches.csv")
+rows = list(csv.reader(open(lpath))) if os.path.exists(lpath) else []
 hdr = None
 tot = defaultdict(float)
 cnt = defaultdict(int)
@@ -38,12 +39,13 @@ for r in rows:
     scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}.get(unit, 1e-6)
     tot[name] += v * scale
     cnt[name] += 1
-all_ms = sum(tot.values())
-lines = ["kernel,launches,total_ms,avg_ms,share"]
-for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-    lines.append(f"{k},{cnt[k]},{v:.3f},{v / cnt[k]:.4f},{v / all_ms:.4f}")
-open(os.path.join(dst, "launch_shares.csv"), "w").write("\n".join(lines) + "\n")
-print("\n".join(lines[:8]))
+if tot:
+    all_ms = sum(tot.values())
+    lines = ["kernel,launches,total_ms,avg_ms,share"]
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+        lines.append(f"{k},{cnt[k]},{v:.3f},{v / cnt[k]:.4f},{v / all_ms:.4f}")
+    open(os.path.join(dst, "launch_shares.csv"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines[:8]))
 
 # ---- full captures
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -89,4 +91,5 @@ for rep in sorted(glob.glob(os.path.join(src, "*.ncu-rep"))):
                  "conv_site_dmma_kernel": "conv_site_kernel", "tt_inner_staged_kernel": "tt_inner_kernel"}.get(short, short)
         traffic[short] = tobytes(d["dram__bytes_read.sum"]) + tobytes(d["dram__bytes_write.sum"])
     print(json.dumps(summ, indent=1))
-json.dump(traffic, open(traffic_path, "w"), indent=1)
+if "--no-traffic" not in sys.argv[3:]:  # secondary captures at other configs leave the bench's traffic alone
+    json.dump(traffic, open(traffic_path, "w"), indent=1)
