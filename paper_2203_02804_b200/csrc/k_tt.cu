@@ -16,7 +16,9 @@
 //        of once per sample.
 #include "ttp_internal.h"
 #include "launch.h"
+#include <cooperative_groups.h>
 #include <cstring>
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -186,6 +188,83 @@ tt_inner_staged_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out,
   }
   if (tid == 0) out[inst] = env[0];
 }
+
+// Bonds above 32 (cfg5, D = 64): the environment and one (env K_s) tile do
+// not leave room to stage slices, and one CTA per instance leaves all but
+// one SM idle for a single option.  A cluster of TS_G CTAs per instance
+// splits each site's s-sum into contiguous chunks (CTA g: s in
+// [g n / G, (g+1) n / G)); every CTA accumulates its partial env' in
+// registers, publishes it in shared memory, and after one cluster barrier
+// every CTA sums the G partials in rank order over DSMEM, so all of them
+// hold the same env' bits for the next site.  Per-CTA arithmetic is that of
+// tt_inner_kernel; the s-sum is grouped by chunk.
+constexpr int TS_G = 16;  // CTAs per instance (non-portable cluster size)
+
+__global__ void __launch_bounds__(INNER_THREADS, 1)
+tt_inner_split_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out, int maxb, int maxk) {
+  extern __shared__ __align__(16) cplx sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = (int)cl.num_blocks();
+  const int g = (int)cl.block_rank();
+  const int inst = blockIdx.x / G;
+  const int tid = threadIdx.x;
+  cplx* env = sm;                 // Db x Dk (full, replicated)
+  cplx* tmp = env + maxb * maxk;  // Db x Dk'
+  cplx* part = tmp + maxb * maxk; // Db' x Dk' partial env' of this CTA
+  if (tid == 0) env[0] = mk(1.0, 0.0);
+  __syncthreads();
+  for (int k = 0; k < bra.d; ++k) {
+    const int Db = bra.bonds[k], Db2 = bra.bonds[k + 1];
+    const int Dk = ket.bonds[k], Dk2 = ket.bonds[k + 1];
+    const int n = bra.shape[k];
+    const cplx* B = bra.cores + inst * bra.stride + bra.off[k];
+    const cplx* K = ket.cores + inst * ket.stride + ket.off[k];
+    const int nacc = Db2 * Dk2;
+    const int s0 = (int)((long long)g * n / G), s1 = (int)((long long)(g + 1) * n / G);
+    cplx acc[INNER_ACC];
+#pragma unroll
+    for (int q = 0; q < INNER_ACC; ++q) acc[q] = mk(0.0, 0.0);
+    for (int s = s0; s < s1; ++s) {
+      for (int e = tid; e < Db * Dk2; e += INNER_THREADS) {
+        const int a = e / Dk2, c = e - a * Dk2;
+        cplx t = mk(0.0, 0.0);
+        for (int b = 0; b < Dk; ++b) t = cfma(env[a * Dk + b], K[((long long)b * n + s) * Dk2 + c], t);
+        tmp[e] = t;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < INNER_ACC; ++q) {
+        const int e = tid + q * INNER_THREADS;
+        if (e < nacc) {
+          const int a2 = e / Dk2, c = e - a2 * Dk2;
+          cplx t = acc[q];
+          for (int a = 0; a < Db; ++a) t = cfmac(B[((long long)a * n + s) * Db2 + a2], tmp[a * Dk2 + c], t);
+          acc[q] = t;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < INNER_ACC; ++q) {
+      const int e = tid + q * INNER_THREADS;
+      if (e < nacc) part[e] = acc[q];
+    }
+    cl.sync();  // every CTA's partial is published
+#pragma unroll
+    for (int q = 0; q < INNER_ACC; ++q) {
+      const int e = tid + q * INNER_THREADS;
+      if (e < nacc) {
+        cplx t = mk(0.0, 0.0);
+        for (int h = 0; h < G; ++h) t = cadd(t, cl.map_shared_rank(part, h)[e]);
+        env[e] = t;
+      }
+    }
+    cl.sync();  // no CTA rewrites its partial while a peer still reads it
+  }
+  if (g == 0 && tid == 0) out[inst] = env[0];
+}
+
+size_t tt_inner_split_smem(int maxb, int maxk) { return sizeof(cplx) * (size_t)(3 * maxb * maxk); }
 
 // FP64 tensor-core variant (DMMA m8n8k4) working on chunks of IC_SC values
 // of s at a time, so each of the two GEMMs per chunk is large enough to keep
@@ -740,6 +819,26 @@ extern "C" int ttp_tt_inner(const ttp_tt_batch* bra, const ttp_tt_batch* ket, do
     LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);
     tt_inner_chunk_kernel<<<bra->n_inst, IC_THREADS, tt_inner_chunk_smem(), (cudaStream_t)stream>>>(
         b, k, reinterpret_cast<cplx*>(d_out));
+  } else if (maxb > 32 || maxk > 32) {
+    // large bonds: the s-sum of each site split over a 16-CTA cluster
+    const size_t ssm = tt_inner_split_smem(maxb, maxk);
+    if (ssm > (size_t)lim) return ttp_fail(TTP_ERR_CAPACITY, "tt_inner: bonds too large for shared memory");
+    TTP_CUDA_CHECK(ensure_max_smem((const void*)tt_inner_split_kernel));
+    TTP_CUDA_CHECK(cudaFuncSetAttribute(tt_inner_split_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(bra->n_inst * TS_G));
+    cfg.blockDim = dim3(INNER_THREADS);
+    cfg.dynamicSmemBytes = ssm;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = TS_G;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);
+    TTP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tt_inner_split_kernel, b, k, reinterpret_cast<cplx*>(d_out), maxb, maxk));
   } else if (smem_staged <= (size_t)lim) {
     TTP_CUDA_CHECK(ensure_max_smem((const void*)tt_inner_staged_kernel));
     LaunchScope _ls(KC_TT_INNER, (cudaStream_t)stream);

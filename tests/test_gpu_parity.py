@@ -81,6 +81,26 @@ def test_p1_contractions_match_reference(golden):
         assert P.tt_rand_sample_diff(a, P.TTOracle(a), 700, 3) <= 1e-13
 
 
+def test_p1_inner_large_bonds_cluster_split():
+    """Bonds above 32 take the cluster-split inner product (the s-sum of a
+    site spread over 16 CTAs): against the CPU oracle, batch == single
+    bitwise, and sites shorter than the cluster (empty chunks)."""
+    rng = np.random.default_rng(11)
+    for phys, bonds in (([5, 40, 9, 3], [1, 5, 64, 27, 1]), ([3, 7, 2, 5, 4], [1, 3, 21, 42, 4, 1])):
+        def rnd():
+            return P.TensorTrain([rng.standard_normal((bonds[k], phys[k], bonds[k + 1]))
+                                  + 1j * rng.standard_normal((bonds[k], phys[k], bonds[k + 1]))
+                                  for k in range(len(phys))])
+        a, b = rnd(), rnd()
+        want = O.tt_inner(a.cores, b.cores)
+        got = P.tt_inner(a, b)
+        assert abs(got - want) <= 1e-12 * abs(want)
+        from paper_2203_02804_b200.tensor_train import DeviceTTBatch
+        batch = P.tt_inner_batch(DeviceTTBatch.from_trains([a, b]), DeviceTTBatch.from_trains([b, b]))
+        assert batch[0] == got
+        assert abs(batch[1] - O.tt_inner(b.cores, b.cores)) <= 1e-12 * abs(batch[1])
+
+
 @pytest.mark.parametrize("cid", [1, 2])
 def test_p1_inner_on_reference_cross_cores(golden, cid):
     """K7 on the reference's own cross cores reproduces the reference's raw sum."""
