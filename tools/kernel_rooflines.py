@@ -33,6 +33,18 @@ elif what == "fiber":
     shape = (spec.grid.points_per_axis,) * spec.d
     b = P.tt_cross_batch([P.PhiGridOracle(m, spec.grid) for m in models], shape, cfg, with_reports=False)
     print("fiber ok", int((b.status == 0).sum()))
+elif what == "inner64":
+    # D = 64 trains (cfg5-like): the cluster-split inner product
+    rng = np.random.default_rng(5)
+    phys, bonds = [257] * 6, [1, 64, 64, 64, 64, 64, 1]
+    def rnd():
+        return P.TensorTrain([rng.standard_normal((bonds[k], phys[k], bonds[k + 1])) + 0j for k in range(6)])
+    a, b = rnd(), rnd()
+    P.tt_inner(a, b)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    v = P.tt_inner(a, b)
+    print("inner64", v, f"{(time.perf_counter() - t1) * 1e3:.1f} ms")
 elif what == "mc":
     models = [configs.make_model(4, i) for i in range(8)]
     res = P.price_monte_carlo_batch(models, 1 << 22, seeds=list(range(8)))

@@ -11,6 +11,7 @@ cap() {  # cap <mode> <ncu -k filter> <name>
   tail -1 $OUT/ncu_$3.log
 }
 cap dense regex:dense_partial dense_partial_kernel
-cap fiber regex:fiber_fast fiber_fast_kernel
+cap fiber "regex:fiber_fast -s 4" fiber_fast_kernel
 cap fiber bond_kernel bond_kernel_v0
 cap mc regex:mc_path mc_path_kernel
+cap inner64 regex:tt_inner_split tt_inner_split_kernel
