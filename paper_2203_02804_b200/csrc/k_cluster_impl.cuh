@@ -854,19 +854,30 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
         // issue the pivot entry and the first KB trailing entries together
         // (the store of the new pivot entry would otherwise order the
         // trailing loads after the pivot load's round trip)
+#ifndef UPD_UB
+#define UPD_UB KB
+#endif
+        constexpr int UB = UPD_UB;  // trailing loads in flight per row chunk
         cplx* prow = c.Ws + l;
-        const long long ld = c.ldw;
+        const int ld = c.ldw;
         const int* cols = c.colmap + i + 1;
-        const int n0 = min(ntr, KB);
-        cplx y[KB];
+        const int n0 = min(ntr, UB);
+        cplx y[UB];
 #pragma unroll
-        for (int u = 0; u < KB; ++u) y[u] = (u < n0) ? prow[cols[u] * ld] : mk(0.0, 0.0);
-        const cplx x = cmul(prow[(long long)ci * ld], scal);
+        for (int u = 0; u < UB; ++u) y[u] = (u < n0) ? prow[cols[u] * ld] : mk(0.0, 0.0);
+        const cplx x = cmul(prow[ci * ld], scal);
 #pragma unroll
-        for (int u = 0; u < KB; ++u)
+        for (int u = 0; u < UB; ++u)
           if (u < n0) prow[cols[u] * ld] = csub(y[u], cmul(x, c.vec[u]));
-        prow[(long long)ci * ld] = x;
-        if (ntr > n0) row_sub_cols(c, cols + n0, c.vec + n0, x, l, ntr - n0);
+        prow[ci * ld] = x;
+        for (int q = n0; q < ntr; q += UB) {
+          const int n1 = min(UB, ntr - q);
+#pragma unroll
+          for (int u = 0; u < UB; ++u) y[u] = (u < n1) ? prow[cols[q + u] * ld] : mk(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < UB; ++u)
+            if (u < n1) prow[cols[q + u] * ld] = csub(y[u], cmul(x, c.vec[q + u]));
+        }
       }
     }
     __syncthreads();
