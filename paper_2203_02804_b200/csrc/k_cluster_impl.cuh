@@ -266,7 +266,10 @@ __device__ __forceinline__ void col_dotc_group(const CC& c, int ci, const int* c
     acc[k] = mk(0.0, 0.0);
   }
   int l = l0;
-  constexpr int RB = (12 / (G + 1)) > 1 ? 12 / (G + 1) : 1;  // ~12 loads in flight
+#ifndef PART_LOADS
+#define PART_LOADS 18
+#endif
+  constexpr int RB = (PART_LOADS / (G + 1)) > 1 ? PART_LOADS / (G + 1) : 1;  // ~PART_LOADS loads in flight
   for (; l + 32 * (RB - 1) < nl; l += 32 * RB) {
     cplx x[RB], y[RB][G];
 #pragma unroll
