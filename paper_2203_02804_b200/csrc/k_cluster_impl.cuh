@@ -675,13 +675,17 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
       for (int q = 0; q < OB; ++q) acc[q] = mk(0.0, 0.0);
       const int amax = min(r, b0 + OB);
       if (g >= r) {
+#ifndef QF_LOADS
+#define QF_LOADS 4
+#endif
+        constexpr int QL = QF_LOADS;  // V loads in flight per row
         int a = 0;
-        for (; a + 4 <= amax; a += 4) {
-          cplx x[4];
+        for (; a + QL <= amax; a += QL) {
+          cplx x[QL];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) x[u] = Wl(c, l, c.colmap[a + u]);
+          for (int u = 0; u < QL; ++u) x[u] = Wl(c, l, c.colmap[a + u]);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < QL; ++u)
 #pragma unroll
             for (int q = 0; q < OB; ++q)
               if (b0 + q < r) acc[q] = cfma(x[u], M[(a + u) * r + b0 + q], acc[q]);

@@ -6,7 +6,7 @@ cp paper_2203_02804_b200/libttpricer_b200.so /tmp/base.so
 for rep in 1 2; do
   cp /tmp/base.so paper_2203_02804_b200/libttpricer_b200.so
   bench base X=1
-  bench lazy2 TTP_LAZY=2
+  [ -n "$LAZY2" ] && bench lazy2 TTP_LAZY=2
   for v in "$@"; do
     cp tools/alt/lib_$v.so paper_2203_02804_b200/libttpricer_b200.so
     bench $v X=1
