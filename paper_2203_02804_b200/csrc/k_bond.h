@@ -59,6 +59,7 @@ struct ClusterJob {
   int fiber_fast;         // src_mode 0: separable evaluation allowed (fiber_fast.cuh)
   int q_wy;               // form Q in compact-WY form (else zung2r rounds)
   int fused_starts;       // both dominant-row starts in one read-only pass sequence
+  int fused_qr;           // column basis: each update pass also forms the next step's partials
   int big;                // bit 0: per-row arrays, bit 1: B[sel,:] in global memory (set by the launcher)
   cplx* Sg;               // global-slice mode: B buffer (holds B[sel,:] in big mode), stride wg_stride
   int debug_start;        // dev aid (TTP_DEBUG_START=1|2): return start set 1 or 2

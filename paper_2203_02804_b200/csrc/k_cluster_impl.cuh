@@ -717,7 +717,48 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
 // ------------------------------------------------------------ phase A
 // Distributed zlaqp2 + zung2r on the block.  Returns false (cluster-uniform)
 // when the block is zero / rank deficient by rank_tol.
-__device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank_tol, bool wy) {
+// conj(y_p) y_t products of 8 columns (v[0..8)) summed over the warp's 32
+// lanes by a transposed butterfly: afterwards lane L holds the sum for
+// column (L >> 2) & 7 (fixed order, 18 shuffles)
+__device__ __forceinline__ cplx warp_transpose_sum8(const cplx* v) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  cplx k4[4], k2[2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const cplx send = b4 ? v[j] : v[j + 4];
+    cplx got;
+    got.x = __shfl_xor_sync(0xffffffffu, send.x, 16);
+    got.y = __shfl_xor_sync(0xffffffffu, send.y, 16);
+    k4[j] = cadd(b4 ? v[j + 4] : v[j], got);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const cplx send = b3 ? k4[j] : k4[j + 2];
+    cplx got;
+    got.x = __shfl_xor_sync(0xffffffffu, send.x, 8);
+    got.y = __shfl_xor_sync(0xffffffffu, send.y, 8);
+    k2[j] = cadd(b3 ? k4[j + 2] : k4[j], got);
+  }
+  cplx k1;
+  {
+    const cplx send = b2 ? k2[0] : k2[1];
+    cplx got;
+    got.x = __shfl_xor_sync(0xffffffffu, send.x, 4);
+    got.y = __shfl_xor_sync(0xffffffffu, send.y, 4);
+    k1 = cadd(b2 ? k2[1] : k2[0], got);
+  }
+#pragma unroll
+  for (int o = 2; o > 0; o >>= 1) {
+    cplx got;
+    got.x = __shfl_xor_sync(0xffffffffu, k1.x, o);
+    got.y = __shfl_xor_sync(0xffffffffu, k1.y, o);
+    k1 = cadd(k1, got);
+  }
+  return k1;
+}
+
+__device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank_tol, bool wy, bool fuse_qr) {
   const int r = c.r, m = c.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lo = c.row0, nl = c.nrows;
@@ -745,7 +786,9 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
     __syncthreads();
   }
   SP_BEGIN(spt);
+  bool fused = false;  // this step's pivot and partials came out of the previous update pass
   for (int i = 0; i < r; ++i) {
+    if (!fused) {
     if (warp == 0) {
       ArgMax am{-1.0, LLONG_MAX};
       for (int j = i + lane; j < r; j += 32)
@@ -761,6 +804,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       }
     }
     __syncthreads();
+    }
     SP(spt, 0);
     const int ci = c.colmap[i];
     const bool own_i = (i >= lo && i < lo + nl);
@@ -768,6 +812,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
     const int lstart = max(0, i + 1 - lo);  // first local row with global index > i
     const int ntr = r - i - 1;
     Rec* me = &c.rec[par];
+    if (!fused) {
     // partials: item 0 = Ssq of x, item g >= 1 = conj(x) . columns i+q for
     // the PG tasks q of group g (column x read once per group; PG sized so
     // that every item gets its own warp)
@@ -806,6 +851,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
           }
         }
       }
+    }
     }
     SP(spt, 1);
     cl.sync();
@@ -850,6 +896,146 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
     par ^= 1;
     __syncthreads();
     SP(spt, 3);
+    int anyflag = 0;
+    for (int q = 0; q < ntr; ++q) anyflag |= c.flags[q];
+    // Fused: when no norm recompute is pending the next pivot is already
+    // known, so this step's update pass also produces the next step's
+    // partials (the reflector's dot products and norm, the pivot row) and
+    // the separate partials pass disappears.
+    fused = fuse_qr && !anyflag && ntr >= 1 && ntr <= 32 && !ident;
+    if (fused) {
+      // pivot of step i+1 (idamax over the downdated norms), swapped into
+      // position i+1 together with its update coefficients
+      if (warp == 0) {
+        ArgMax am{-1.0, LLONG_MAX};
+        for (int j = i + 1 + lane; j < r; j += 32)
+          if (argmax_better(c.cn1[j], j, am.v, am.key)) am = ArgMax{c.cn1[j], j};
+        am = warp_argmax(am);
+        const int p = (int)am.key;
+        if (lane == 0 && p != i + 1) {
+          const int t = c.colmap[p];
+          c.colmap[p] = c.colmap[i + 1];
+          c.colmap[i + 1] = t;
+          c.cn1[p] = c.cn1[i + 1];
+          c.cn2[p] = c.cn2[i + 1];
+          const int qa = 0, qb = p - i - 1;
+          const cplx va = c.vec[qa], wa = c.vec2[qa];
+          c.vec[qa] = c.vec[qb];
+          c.vec2[qa] = c.vec2[qb];
+          c.vec[qb] = va;
+          c.vec2[qb] = wa;
+        }
+      }
+      __syncthreads();
+      const int* cols = c.colmap + i + 1;  // cols[0]: pivot of step i+1
+      const int nch = (ntr + 7) / 8;  // <= 4
+      const int ldw = c.ldw;
+      Rec* nx = &c.rec[par];  // step i+1's record
+      cplx acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = mk(0.0, 0.0);
+      double s2 = 0.0, mx = 0.0;
+      const int nk = (nl + CT - 1) / CT;
+      const bool rev = g_serpentine && (i & 1) == 0;
+      for (int k = 0; k < nk; ++k) {
+        const int l = threadIdx.x + (rev ? nk - 1 - k : k) * CT;
+        const bool act = l < nl;
+        const int g = lo + l;
+        cplx* prow = c.Ws + (act ? l : 0);
+        if (act && g == i) {
+          prow[ci * ldw] = mk(h.beta, 0.0);
+          for (int q = 1; q <= ntr; ++q) prow[cols[q - 1] * ldw] = c.vec2[q - 1];
+        }
+        const bool upd = act && g > i;
+        const bool prod = act && g > i + 1;
+        cplx x = mk(0.0, 0.0), yp = mk(0.0, 0.0);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          if (ch < nch) {
+            const int t0 = ch * 8;
+            cplx y[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) y[u] = (upd && t0 + u < ntr) ? prow[cols[t0 + u] * ldw] : mk(0.0, 0.0);
+            if (ch == 0) {
+              if (upd) x = cmul(prow[ci * ldw], scal);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (upd && t0 + u < ntr) {
+                y[u] = csub(y[u], cmul(x, c.vec[t0 + u]));
+                prow[cols[t0 + u] * ldw] = y[u];
+              }
+            if (ch == 0) {
+              if (upd) prow[ci * ldw] = x;
+              yp = y[0];
+              if (prod) {
+                s2 = fma(yp.x, yp.x, fma(yp.y, yp.y, s2));
+                mx = fmax(mx, fmax(fabs(yp.x), fabs(yp.y)));
+              }
+              if (act && g == i + 1) {
+                nx->data[1] = yp;
+                for (int u = 1; u < 8; ++u)
+                  if (u < ntr) nx->data[1 + r + u] = y[u];
+              }
+            } else if (act && g == i + 1) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (t0 + u < ntr) nx->data[1 + r + t0 + u] = y[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              y[u] = (prod && t0 + u < ntr && t0 + u > 0) ? cmulc(yp, y[u]) : mk(0.0, 0.0);
+            acc[ch] = cadd(acc[ch], warp_transpose_sum8(y));
+          }
+        }
+      }
+      // per-warp partials -> shared memory, then every CTA's record in
+      // warp order (lanes 4v hold column v of each chunk)
+      cplx* part = c.wrow;  // CW x r, free during the column basis
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const int t = ch * 8 + (lane >> 2);
+        if (ch < nch && (lane & 3) == 0 && t < ntr) part[warp * r + t] = acc[ch];
+      }
+      s2 = warp_sum(s2);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) c.wss[warp] = Ssq{mx, s2};
+      __syncthreads();
+      if (warp == 0) {
+        for (int t = 1 + lane; t < ntr; t += 32) {
+          cplx d = mk(0.0, 0.0);
+          for (int w = 0; w < CW; ++w) d = cadd(d, part[w * r + t]);
+          nx->data[1 + t] = d;
+        }
+        const bool own_n = (i + 1 >= lo && i + 1 < lo + nl);
+        if (!own_n) {
+          if (lane == 0) nx->data[1] = mk(0.0, 0.0);
+          for (int t = 1 + lane; t < ntr; t += 32) nx->data[1 + r + t] = mk(0.0, 0.0);
+        }
+        double sum = 0.0, m2 = 0.0;
+        for (int w = 0; w < CW; ++w) {
+          sum += c.wss[w].ssq;
+          m2 = fmax(m2, c.wss[w].scale);
+        }
+        if (m2 == 0.0) {
+          if (lane == 0) nx->data[0] = mk(0.0, 1.0);
+        } else if (m2 > 1e-140 && m2 < 1e140) {
+          if (lane == 0) nx->data[0] = mk(1.0, sum);  // scale 1: the plain sum of squares
+        } else {
+          // out of the safe range: the scaled two-pass sum of squares
+          const int cpn = cols[0];
+          const int ls2 = max(0, i + 2 - lo);
+          const int f0 = ls2 + lane;
+          Ssq sq = ssq_of(&c.Ws[(long long)cpn * ldw + f0], 32, nl > f0 ? (nl - f0 + 31) / 32 : 0);
+          sq = warp_ssq(sq);
+          if (lane == 0) nx->data[0] = mk(sq.scale, sq.ssq);
+        }
+      }
+      __syncthreads();
+      SP(spt, 4);
+      continue;
+    }
     // local update of my rows (descending: the partials pass ran ascending)
     FOR_MY_ROWS(l, nl, g_serpentine) {
       const int g = lo + l;
@@ -890,8 +1076,6 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
     __syncthreads();
     SP(spt, 4);
     // norm recompute round (only if some column flagged; replicated decision)
-    int anyflag = 0;
-    for (int q = 0; q < ntr; ++q) anyflag |= c.flags[q];
     if (anyflag) {
       Rec* me2 = &c.rec[par];
       for (int q = warp; q < ntr; q += CW) {
@@ -1939,7 +2123,7 @@ __global__ void __launch_bounds__(CT, CLUSTER_MIN_BLOCKS) cluster_bond_kernel(Cl
   PHASE_MARK(0);
   load_block(c, J, inst);
   PHASE_MARK(1);
-  if (!column_basis(cl, c, par, job.rank_tol, J.q_wy != 0)) {
+  if (!column_basis(cl, c, par, job.rank_tol, J.q_wy != 0, J.fused_qr != 0)) {
     if (c.crank == 0 && threadIdx.x == 0) set_error(job, inst, TTP_ERR_SINGULAR);
     cl.sync();
     return;
@@ -2203,8 +2387,20 @@ static cudaError_t apply_lazy_knob() {
   return st;
 }
 
+// TTP_FUSED_QR=0 runs the column basis with a separate partials pass per
+// step (A/B knob); default: each update pass also produces the next step's
+// partials.
+static bool fused_qr_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TTP_FUSED_QR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream_t s) {
   ClusterJob job = job_in;
+  job.fused_qr = fused_qr_enabled() ? 1 : 0;
   {
     const cudaError_t e = apply_lazy_knob();
     if (e != cudaSuccess) return e;

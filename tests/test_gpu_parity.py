@@ -439,7 +439,10 @@ np.savez(sys.argv[1], *[c for i in (0, 8, 16) for c in tr[i].cores])
 def test_throughput_and_latency_cluster_kernels_agree(tmp_path):
     """A cfg4 batch of 17 (global-slice clusters) gives the same cores
     bitwise from the 256-thread two-CTAs-per-SM instantiation and the
-    512-thread one (TTP_CK forces each in its own process)."""
+    512-thread one (TTP_CK forces each in its own process).  The column
+    basis runs with separate partials passes here (TTP_FUSED_QR=0): the
+    fused update pass sums its dot products per warp, so its rounding
+    depends on the CTA width."""
     import os
     import subprocess
     import sys
@@ -447,7 +450,7 @@ def test_throughput_and_latency_cluster_kernels_agree(tmp_path):
     script.write_text(_CK_SCRIPT)
     out = {}
     for ck in ("tp", "lat"):
-        env = dict(os.environ, TTP_CK=ck)
+        env = dict(os.environ, TTP_CK=ck, TTP_FUSED_QR="0")
         path = tmp_path / f"{ck}.npz"
         subprocess.run([sys.executable, str(script), str(path)], check=True, env=env,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
