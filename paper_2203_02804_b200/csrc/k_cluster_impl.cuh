@@ -758,6 +758,27 @@ __device__ __forceinline__ cplx warp_transpose_sum8(const cplx* v) {
   return k1;
 }
 
+// 16-column version: lane L ends with the sum for column (L >> 1) & 15
+__device__ __forceinline__ cplx warp_transpose_sum16(const cplx* v) {
+  const int lane = threadIdx.x & 31;
+  cplx k8[8], k4[4], k2[2];
+  auto xch = [](cplx send, int o) {
+    cplx got;
+    got.x = __shfl_xor_sync(0xffffffffu, send.x, o);
+    got.y = __shfl_xor_sync(0xffffffffu, send.y, o);
+    return got;
+  };
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) k8[j] = cadd(b4 ? v[j + 8] : v[j], xch(b4 ? v[j] : v[j + 8], 16));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) k4[j] = cadd(b3 ? k8[j + 4] : k8[j], xch(b3 ? k8[j] : k8[j + 4], 8));
+#pragma unroll
+  for (int j = 0; j < 2; ++j) k2[j] = cadd(b2 ? k4[j + 2] : k4[j], xch(b2 ? k4[j] : k4[j + 2], 4));
+  cplx k1 = cadd(b1 ? k2[1] : k2[0], xch(b1 ? k2[0] : k2[1], 2));
+  return cadd(k1, xch(k1, 1));
+}
+
 __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank_tol, bool wy, bool fuse_qr) {
   const int r = c.r, m = c.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -928,12 +949,17 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       }
       __syncthreads();
       const int* cols = c.colmap + i + 1;  // cols[0]: pivot of step i+1
-      const int nch = (ntr + 7) / 8;  // <= 4
+#ifndef FQ_CH
+#define FQ_CH 8
+#endif
+      constexpr int FQ = FQ_CH;        // trailing entries per chunk (loads in flight)
+      constexpr int NCH = 32 / FQ;
+      const int nch = (ntr + FQ - 1) / FQ;  // <= NCH
       const int ldw = c.ldw;
       Rec* nx = &c.rec[par];  // step i+1's record
-      cplx acc[4];
+      cplx acc[NCH];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = mk(0.0, 0.0);
+      for (int u = 0; u < NCH; ++u) acc[u] = mk(0.0, 0.0);
       double s2 = 0.0, mx = 0.0;
       const int nk = (nl + CT - 1) / CT;
       const bool rev = g_serpentine && (i & 1) == 0;
@@ -950,17 +976,17 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
         const bool prod = act && g > i + 1;
         cplx x = mk(0.0, 0.0), yp = mk(0.0, 0.0);
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        for (int ch = 0; ch < NCH; ++ch) {
           if (ch < nch) {
-            const int t0 = ch * 8;
-            cplx y[8];
+            const int t0 = ch * FQ;
+            cplx y[FQ];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) y[u] = (upd && t0 + u < ntr) ? prow[cols[t0 + u] * ldw] : mk(0.0, 0.0);
+            for (int u = 0; u < FQ; ++u) y[u] = (upd && t0 + u < ntr) ? prow[cols[t0 + u] * ldw] : mk(0.0, 0.0);
             if (ch == 0) {
               if (upd) x = cmul(prow[ci * ldw], scal);
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < FQ; ++u)
               if (upd && t0 + u < ntr) {
                 y[u] = csub(y[u], cmul(x, c.vec[t0 + u]));
                 prow[cols[t0 + u] * ldw] = y[u];
@@ -974,18 +1000,19 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
               }
               if (act && g == i + 1) {
                 nx->data[1] = yp;
-                for (int u = 1; u < 8; ++u)
+                for (int u = 1; u < FQ; ++u)
                   if (u < ntr) nx->data[1 + r + u] = y[u];
               }
             } else if (act && g == i + 1) {
 #pragma unroll
-              for (int u = 0; u < 8; ++u)
+              for (int u = 0; u < FQ; ++u)
                 if (t0 + u < ntr) nx->data[1 + r + t0 + u] = y[u];
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < FQ; ++u)
               y[u] = (prod && t0 + u < ntr && t0 + u > 0) ? cmulc(yp, y[u]) : mk(0.0, 0.0);
-            acc[ch] = cadd(acc[ch], warp_transpose_sum8(y));
+            if constexpr (FQ == 16) acc[ch] = cadd(acc[ch], warp_transpose_sum16(y));
+            else acc[ch] = cadd(acc[ch], warp_transpose_sum8(y));
           }
         }
       }
@@ -993,9 +1020,11 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
       // warp order (lanes 4v hold column v of each chunk)
       cplx* part = c.wrow;  // CW x r, free during the column basis
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        const int t = ch * 8 + (lane >> 2);
-        if (ch < nch && (lane & 3) == 0 && t < ntr) part[warp * r + t] = acc[ch];
+      for (int ch = 0; ch < NCH; ++ch) {
+        // lane L holds column (L >> 2) & 7 (8-wide chunks) or (L >> 1) & 15
+        const int sh = FQ == 16 ? 1 : 2;
+        const int t = ch * FQ + (lane >> sh);
+        if (ch < nch && (lane & ((1 << sh) - 1)) == 0 && t < ntr) part[warp * r + t] = acc[ch];
       }
       s2 = warp_sum(s2);
 #pragma unroll
