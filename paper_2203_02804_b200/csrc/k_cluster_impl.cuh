@@ -1908,7 +1908,10 @@ __device__ __forceinline__ Cand swap_pass(const CC& c, const cplx* pw, const int
     int t = 0;
     // the hottest loop: 16 loads in flight (8 with three or more pending
     // updates, whose coefficients take the registers)
-    constexpr int KS = NP <= 2 ? 2 * KB : KB;
+#ifndef SW_KS34
+#define SW_KS34 KB
+#endif
+    constexpr int KS = NP <= 2 ? 2 * KB : SW_KS34;
     for (; t + KS <= r; t += KS) {
       cplx x[KS];
 #pragma unroll
