@@ -37,3 +37,23 @@ timed("oracle batches from models", lambda: (P.OracleBatch([P.PhiGridOracle(m, g
                                               P.OracleBatch([P.PayoffGridOracle(m, grid, conj=True) for m in models])))
 timed("price_fourier_tt_batch", lambda: P.price_fourier_tt_batch(models, grid, cfg, cfg, dense_reference="never"))
 timed("price_fourier_tt_batch_capi", lambda: price_fourier_tt_batch_capi(models, grid, cfg, cfg))
+
+# segment timing of one public call
+import paper_2203_02804_b200.pricers as PR  # noqa: E402
+t0 = time.perf_counter()
+ob = (P.OracleBatch([P.PhiGridOracle(m, grid) for m in models]), P.OracleBatch([P.PayoffGridOracle(m, grid, conj=True) for m in models]))
+t1 = time.perf_counter()
+rp, rv = run_cross_pair(ob[0], ob[1], shape, cfg, cfg)
+torch.cuda.synchronize()
+t2 = time.perf_counter()
+raw = P.tt_inner_batch(rv.trains, rp.trains)
+t3 = time.perf_counter()
+res = []
+for i, m in enumerate(models):
+    err = rp.error_for(i) or rv.error_for(i)
+    value = PR._prefactor(m, grid, 0.0) * raw[i]
+    diag = {"cross_phi": rp.reports[i], "cross_v": rv.reports[i], "imag_part": float(value.imag),
+            "oracle_calls_total": rp.reports[i].oracle_calls + rv.reports[i].oracle_calls}
+    res.append(PR.PricingResult(float(value.real), "fourier_tt", 0.0, diag))
+t4 = time.perf_counter()
+print(f"oracles {1e3*(t1-t0):.1f} ms, crosses {1e3*(t2-t1):.1f} ms, inner {1e3*(t3-t2):.1f} ms, results {1e3*(t4-t3):.1f} ms")
