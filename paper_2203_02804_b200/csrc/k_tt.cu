@@ -275,8 +275,15 @@ size_t tt_inner_split_smem(int maxb, int maxk) { return sizeof(cplx) * (size_t)(
 // conjugate sign for B; right operands expanded on the fly).  E lives in the
 // DMMA accumulators for the whole site.  Core slices of the next chunk stream
 // in by cp.async while the current one is contracted.  Bonds <= 32.
-constexpr int IC_SC = 2;
-constexpr int IC_THREADS = 512;
+#ifndef IC_SC_DEF
+#define IC_SC_DEF 2
+#endif
+#ifndef IC_THREADS_DEF
+#define IC_THREADS_DEF 512
+#endif
+constexpr int IC_SC = IC_SC_DEF;            // s values per chunk
+constexpr int IC_THREADS = IC_THREADS_DEF;  // 512 (one CTA per SM) or 256
+constexpr int IC_MINB = IC_THREADS >= 512 ? 1 : 2;
 
 __device__ __forceinline__ void ic_dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -291,7 +298,7 @@ __device__ __forceinline__ double ic_gexp(const cplx* G, int ldg, int rows, int 
   return ((k & 1) == (n & 1)) ? g.x : ((n & 1) ? g.y : -g.y);
 }
 
-__global__ void __launch_bounds__(IC_THREADS, 1)
+__global__ void __launch_bounds__(IC_THREADS, IC_MINB)
 tt_inner_chunk_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) {
   extern __shared__ __align__(16) cplx sm[];
   constexpr int MX = 32;
@@ -299,6 +306,7 @@ tt_inner_chunk_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   constexpr int NW = IC_THREADS / 32;
+  static_assert(NW == 8 || NW == 16, "GEMM2 tiling assumes 8 or 16 warps");
   const int ldE = 2 * MX + 4;
   double* envd = reinterpret_cast<double*>(sm);                 // MX x ldE
   cplx* T = reinterpret_cast<cplx*>(envd + MX * ldE);            // MX x SC*MX
@@ -337,10 +345,13 @@ tt_inner_chunk_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) 
       }
       asm volatile("cp.async.commit_group;\n" ::);
     };
-    // GEMM2 output tiles: n-tile (warp & 7) of 2*Dk2, m-tiles (warp >> 3) + 2i of Db2
+    // GEMM2 output tiles: n-tile (warp & 7) of 2*Dk2, m-tiles (warp >> 3) + MG*i of Db2
+    constexpr int MG = NW / 8, MPW = 4 / MG;  // warp groups over the 4 m-tiles; m-tiles per warp
     const int ntn2 = (2 * Dk2 + 7) / 8, mtn2 = (Db2 + 7) / 8;
     const int nt2 = warp & 7, mg2 = warp >> 3;
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double acc[MPW][2];
+#pragma unroll
+    for (int i = 0; i < MPW; ++i) acc[i][0] = acc[i][1] = 0.0;
     issue(0, 0);
     for (int ch = 0; ch < nch; ++ch) {
       const int buf = ch & 1;
@@ -387,8 +398,8 @@ tt_inner_chunk_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) 
           const int a = kap / IC_SC, sl = kap - a * IC_SC;
           const double bv = ic_gexp(T, Dk2, kdim, Dk2, kx, nt2 * 8 + gid);
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int mt = mg2 + 2 * i;
+          for (int i = 0; i < MPW; ++i) {
+            const int mt = mg2 + MG * i;
             if (mt < mtn2) {
               const int a2 = mt * 8 + gid;
               double av = 0.0;
@@ -408,8 +419,8 @@ tt_inner_chunk_kernel(const TTDev bra, const TTDev ket, cplx* __restrict__ out) 
     __syncthreads();
     if (nt2 < ntn2) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int mt = mg2 + 2 * i;
+      for (int i = 0; i < MPW; ++i) {
+        const int mt = mg2 + MG * i;
         const int row = mt * 8 + gid, col = (nt2 * 8 + 2 * tig) >> 1;
         if (mt < mtn2 && row < Db2 && col < Dk2) {
           envd[row * ldE + 2 * col] = acc[i][0];
