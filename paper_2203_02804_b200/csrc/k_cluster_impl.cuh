@@ -13,17 +13,26 @@
 // order -- so all CTAs take bitwise-identical decisions with no second
 // round and no global-memory traffic on the critical path.
 //
+// Global-slice mode (ClusterJob.Wg set; every throughput batch of blocks
+// >= 1 MB): the row slices live in global memory instead (L2/HBM), only the
+// small state stays in shared memory, and clusters of 2 CTAs keep 74
+// (512-thread instantiation) or 148 (256-thread, two per SM) instances in
+// flight.  Peers then read a swap winner's row straight from its owner's
+// slice, ordered against the owner's rewrites by a split cluster barrier.
+//
 // Phases per bond (reference decision order, as in k_bond_v0.cu):
 //   0  fibers: the oracle is evaluated straight into shared memory (no HBM
 //      round trip for the sampled block; pricers.py:234-253 via cross.py:310-332)
 //   A  zgeqp3 (zlaqp2: pivot, zlarfg, zlarf, partial-norm downdate/recompute)
-//      + zung2r, distributed: 1 round per step (+1 when a norm recompute fires)
-//      -> orthonormal Q (written once to global, L2-resident)       cross.py:103-119
-//   B  start 1: zlaqp2 on Q^H (right-looking, reflectors of length r)  cross.py:184-185
-//   C  start 2: zgetrf partial pivoting (|Re|+|Im|)                  cross.py:186-187
+//      distributed: 1 round per step (+1 when a norm recompute fires); each
+//      step's update pass also forms the next step's partials (fused QR);
+//      Q in compact-WY form -> orthonormal Q (global, L2-resident)  cross.py:103-119
+//   B+C both starts fused in one read-only pass per round over Q: zlaqp2 on
+//      Q^H and zgetrf partial pivoting (|Re|+|Im|)                 cross.py:184-187
 //   D  _swap_to_dominance from each start; every CTA keeps a replicated
-//      copy of B[sel, :] so the rank-1 update needs only the winning row,
-//      which travels with the argmax record                        cross.py:122-139
+//      copy of B[sel, :] so the rank-1 update needs only the winning row;
+//      in global-slice mode up to 4 rank-1 updates are deferred into
+//      read-only row passes (bitwise the eager values)             cross.py:122-139
 //   E  slogdet choice, cond screen, factor Q Q[sel]^-1 -> TT core     cross.py:191-205,349-355
 //
 // This file is compiled twice (k_cluster.cu, k_cluster_tp.cu) with different
