@@ -113,3 +113,16 @@ def test_tt_prices_bitwise(golden, cid, inst):
     assert info["cross_phi"]["final_diff"] == ref["cross_phi"]["final_diff"]
     assert info["cross_v"]["oracle_calls"] == ref["cross_v"]["oracle_calls"]
     assert sets_as_lists(info["cross_phi"]["left"]) == ref["cross_phi"]["left_sets"]
+
+
+def test_cfg4_noise_band_fixture_is_pinned(golden):
+    """The band fixture behind the cfg4 P4 tolerance starts from the
+    reference's own cfg4 price (unperturbed run == golden, bitwise) and its
+    perturbed runs all stay within the band the GPU tests use."""
+    import json
+    import os
+    from conftest import GOLDEN
+    band = json.load(open(os.path.join(GOLDEN, "cfg4_noise_band.json")))
+    assert band["unperturbed"] == golden["prices"]["cfg4_i0"]["price"]
+    assert len(band["rel_dev_sorted"]) >= 10
+    assert max(band["rel_dev_sorted"]) <= 4e-5
