@@ -31,7 +31,8 @@ size_t conv_site_smem(int ra, int rb, int threads);
 int conv_site_dmma_nt(int rb);
 cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long offk, int ra, int n,
                                   int rb, const int* perm, const int* goff, const cplx* vin, cplx* vout,
-                                  long long vstride, const int* active, int n_inst, cudaStream_t s);
+                                  long long vstride, const int* active, int n_inst, cudaStream_t s,
+                                  long long off0 = 0, const int* idx0 = nullptr, int idx_d = 0);
 
 // TTP_CONV_DMMA=0 selects the scalar-FMA site kernel (A/B checks).
 bool conv_dmma_enabled() {
@@ -327,7 +328,10 @@ int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const 
   const long long M = P.cfg.n_conv_samples;
   const cplx* cores = reinterpret_cast<const cplx*>(out.d_cores);
   const int r1 = L.ranks[1];
-  {
+  // site 1 on the DMMA path gathers its input rows straight from the first
+  // core (row i_0 of each sample), so the site-0 rows are not materialised
+  const bool gather0 = d >= 2 && conv_dmma_enabled() && conv_site_dmma_nt(L.ranks[2]) > 0;
+  if (!gather0) {
     const long long tot = M * r1;
     dim3 grid((unsigned)((tot + 255) / 256), (unsigned)n);
     {
@@ -344,9 +348,11 @@ int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const 
       const int ra = L.ranks[k], rb = L.ranks[k + 1], nk = P.h_shape[k];
       if (conv_dmma_enabled() && conv_site_dmma_nt(rb) > 0) {
         LaunchScope _ls(KC_CONV_SITE, s);
+        const bool g0 = gather0 && k == 1;
         TTP_CUDA_CHECK(launch_conv_site_dmma(cores, L.core_stride, L.core_offsets[k], ra, nk, rb,
                                              P.d_conv_perm + (long long)k * M, P.d_conv_off + goff, vin,
-                                             vout, w.v_stride, d_active, n, s));
+                                             vout, w.v_stride, d_active, n, s, L.core_offsets[0],
+                                             g0 ? P.d_conv_idx : nullptr, d));
         std::swap(vin, vout);
         goff += P.h_shape[k] + 1;
         continue;

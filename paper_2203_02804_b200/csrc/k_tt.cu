@@ -591,11 +591,12 @@ __device__ __forceinline__ double cd_bfrag(const cplx* G, int ra, int rb, int k0
 
 // KS > 0: all KS x NT B' fragments of the warp live in registers (formed
 // once per CTA); KS == 0: formed per k-step from the complex slice.
-template <int NT, int KS>
+template <int NT, int KS, bool G0>
 __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
     const cplx* __restrict__ cores, long long stride, long long offk, int ra, int n, int rb,
     const int* __restrict__ perm, const int* __restrict__ goff, const cplx* __restrict__ Vin,
-    cplx* __restrict__ Vout, long long vstride, const int* __restrict__ active) {
+    cplx* __restrict__ Vout, long long vstride, const int* __restrict__ active,
+    long long off0, const int* __restrict__ idx0, int idx_d) {
   extern __shared__ __align__(16) double cd_smem[];
   const int inst = blockIdx.y;
   if (active && !active[inst]) return;
@@ -611,6 +612,9 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
   int* rowj = reinterpret_cast<int*>(stage1 + CD_ROWS * KP);  // [2][CD_ROWS]
   const cplx* vin = Vin + inst * vstride;
   cplx* vout = Vout + inst * vstride;
+  // site 1 (idx0 set): a sample's input row is row i_0 of the first core,
+  // gathered straight from it (no materialised site-0 rows)
+  const cplx* core0 = cores + inst * stride + off0;
   const int ntile = (g1 - g0 + CD_ROWS - 1) / CD_ROWS;
   // gather of one tile: CD_THREADS / CD_ROWS threads per row, each loading
   // the row's sample index once and copying every TPR-th 16-byte chunk
@@ -618,20 +622,27 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
   constexpr int TPR = CD_THREADS / CD_ROWS;
   const int grow = threadIdx.x / TPR, gcg = threadIdx.x - grow * TPR;
   auto sample_j = [&](int tile) { return tile < ntile ? perm[min(g0 + tile * CD_ROWS + grow, g1 - 1)] : 0; };
-  auto issue = [&](int tile, int buf, int j) {
+  // i0 >= 0: the sample's first-core row, already loaded (site-1 mode)
+  auto issue = [&](int tile, int buf, int j, int i0) {
     double* st = buf ? stage1 : stage0;
     int* rj = rowj + buf * CD_ROWS;
     const int t0 = g0 + tile * CD_ROWS;
     const int row = grow, cg = gcg;
     if (cg == 0) rj[row] = (t0 + row < g1) ? j : -1;
-    const cplx* srow = vin + (long long)j * ra;
+    const cplx* srow;
+    if constexpr (G0) {
+      if (i0 < 0) i0 = idx0[(long long)j * idx_d];
+      srow = core0 + (long long)i0 * ra;
+    } else {
+      srow = vin + (long long)j * ra;
+    }
     const unsigned dst = (unsigned)__cvta_generic_to_shared(st + row * KP);
     for (int ch = cg; ch < ra; ch += TPR)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * ch), "l"(srow + ch));
     cp_async_commit();
   };
-  issue(0, 0, sample_j(0));  // first gather overlaps the slice load below
-  int jnext = sample_j(1);
+  issue(0, 0, sample_j(0), -1);  // first gather overlaps the slice load below
+  int jnext = sample_j(1), inext = -1;
   const cplx* src = cores + inst * stride + offk;
   for (int e = threadIdx.x; e < ra * rb; e += CD_THREADS) {
     const int a = e / rb, c = e - a * rb;
@@ -658,8 +669,9 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
   for (int tile = 0; tile < ntile; ++tile) {
     const int buf = tile & 1;
     if (tile + 1 < ntile) {
-      issue(tile + 1, buf ^ 1, jnext);
+      issue(tile + 1, buf ^ 1, jnext, inext);
       jnext = sample_j(tile + 2);
+      inext = -1;
       cp_async_wait_all_but_one();
     } else {
       cp_async_wait_all();
@@ -702,6 +714,9 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
                          : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1]) : "d"(av[mt]), "d"(bv[nt]));
       }
     }
+    if constexpr (G0) {
+      if (tile + 2 < ntile) inext = idx0[(long long)jnext * idx_d];  // jnext has landed by now
+    }
     // c0, c1 = C'[row][2 tig], C'[row][2 tig + 1] = one complex output
 #pragma unroll
     for (int mt = 0; mt < CD_MT; ++mt) {
@@ -730,7 +745,8 @@ int conv_site_dmma_nt(int rb) {
 
 cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long offk, int ra, int n,
                                   int rb, const int* perm, const int* goff, const cplx* vin, cplx* vout,
-                                  long long vstride, const int* active, int n_inst, cudaStream_t s) {
+                                  long long vstride, const int* active, int n_inst, cudaStream_t s,
+                                  long long off0, const int* idx0, int idx_d) {
   const int nt = conv_site_dmma_nt(rb);
   const size_t smem = conv_site_dmma_smem(ra, rb);
   dim3 grid((unsigned)n, (unsigned)n_inst);
@@ -740,11 +756,17 @@ cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long
   const int code = nt * 100 + ((ks > 0 && ks * nt <= 32) ? ks : 0);
 #define CD_CASE(NT, KS)                                                                          \
   case NT * 100 + KS: {                                                                          \
-    cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS>);                 \
-    if (e != cudaSuccess) return e;                                                              \
-    conv_site_dmma_kernel<NT, KS><<<grid, CD_THREADS, smem, s>>>(cores, stride, offk, ra, n, rb, \
-                                                                  perm, goff, vin, vout, vstride, \
-                                                                  active);                       \
+    if (idx0) {                                                                                  \
+      cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS, true>);         \
+      if (e != cudaSuccess) return e;                                                            \
+      conv_site_dmma_kernel<NT, KS, true><<<grid, CD_THREADS, smem, s>>>(                        \
+          cores, stride, offk, ra, n, rb, perm, goff, vin, vout, vstride, active, off0, idx0, idx_d); \
+    } else {                                                                                     \
+      cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS, false>);        \
+      if (e != cudaSuccess) return e;                                                            \
+      conv_site_dmma_kernel<NT, KS, false><<<grid, CD_THREADS, smem, s>>>(                       \
+          cores, stride, offk, ra, n, rb, perm, goff, vin, vout, vstride, active, off0, idx0, idx_d); \
+    }                                                                                            \
     break;                                                                                       \
   }
   switch (code) {
