@@ -32,7 +32,8 @@ int conv_site_dmma_nt(int rb);
 cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long offk, int ra, int n,
                                   int rb, const int* perm, const int* goff, const cplx* vin, cplx* vout,
                                   long long vstride, const int* active, int n_inst, cudaStream_t s,
-                                  long long off0 = 0, const int* idx0 = nullptr, int idx_d = 0);
+                                  long long off0 = 0, const int* idx0 = nullptr, int idx_d = 0,
+                                  int mode = 0, int n0 = 0);
 
 // TTP_CONV_DMMA=0 selects the scalar-FMA site kernel (A/B checks).
 bool conv_dmma_enabled() {
@@ -342,17 +343,23 @@ int run_conv_check(const ttp_cross_problem& P, const ttp_cross_layout& L, const 
   }
   cplx* vin = w.V0;
   cplx* vout = w.V1;
+  // site 1 as a dense (i_1, i_0) table when that has fewer rows than the
+  // sample set (cfg1-4): one product per pair, written over V0 (free, since
+  // site 0 is not materialised); site 2 gathers from it
+  const long long tab_rows = d >= 3 ? (long long)P.h_shape[0] * P.h_shape[1] : 0;
+  const bool table = gather0 && d >= 3 && tab_rows <= M && conv_site_dmma_nt(L.ranks[3]) > 0;
+  if (table) std::swap(vin, vout);  // site 1 writes V0, site 2 reads it
   long long goff = 0;
   for (int k = 0; k < d; ++k) {
     if (k >= 1) {
       const int ra = L.ranks[k], rb = L.ranks[k + 1], nk = P.h_shape[k];
       if (conv_dmma_enabled() && conv_site_dmma_nt(rb) > 0) {
         LaunchScope _ls(KC_CONV_SITE, s);
-        const bool g0 = gather0 && k == 1;
+        const int mode = (gather0 && k == 1) ? (table ? 2 : 1) : (table && k == 2) ? 3 : 0;
         TTP_CUDA_CHECK(launch_conv_site_dmma(cores, L.core_stride, L.core_offsets[k], ra, nk, rb,
                                              P.d_conv_perm + (long long)k * M, P.d_conv_off + goff, vin,
                                              vout, w.v_stride, d_active, n, s, L.core_offsets[0],
-                                             g0 ? P.d_conv_idx : nullptr, d));
+                                             P.d_conv_idx, d, mode, P.h_shape[0]));
         std::swap(vin, vout);
         goff += P.h_shape[k] + 1;
         continue;

@@ -591,17 +591,26 @@ __device__ __forceinline__ double cd_bfrag(const cplx* G, int ra, int rb, int k0
 
 // KS > 0: all KS x NT B' fragments of the warp live in registers (formed
 // once per CTA); KS == 0: formed per k-step from the complex slice.
-template <int NT, int KS, bool G0>
+// Gather modes of the site kernel:
+//   CD_PLAIN  row j of Vin (the previous site's sample vectors)
+//   CD_G0     site 1: row i_0(j) of the first core (site-0 vectors are core rows)
+//   CD_TAB1   site 1 as a table: every first-core row t of the bucket s, output
+//             row s * n0 + t of Vout (one product per (i_1, i_0) pair instead
+//             of one per sample; used when n0 * n1 <= the sample count)
+//   CD_TAB2   site 2 from that table: row i_1(j) * n0 + i_0(j) of Vin
+constexpr int CD_PLAIN = 0, CD_G0 = 1, CD_TAB1 = 2, CD_TAB2 = 3;
+
+template <int NT, int KS, int MODE>
 __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
     const cplx* __restrict__ cores, long long stride, long long offk, int ra, int n, int rb,
     const int* __restrict__ perm, const int* __restrict__ goff, const cplx* __restrict__ Vin,
     cplx* __restrict__ Vout, long long vstride, const int* __restrict__ active,
-    long long off0, const int* __restrict__ idx0, int idx_d) {
+    long long off0, const int* __restrict__ idx0, int idx_d, int n0) {
   extern __shared__ __align__(16) double cd_smem[];
   const int inst = blockIdx.y;
   if (active && !active[inst]) return;
   const int s = blockIdx.x;
-  const int g0 = goff[s], g1 = goff[s + 1];
+  const int g0 = MODE == CD_TAB1 ? 0 : goff[s], g1 = MODE == CD_TAB1 ? n0 : goff[s + 1];
   if (g0 >= g1) return;
   const int KP = cd_kp(ra);
   const int K2 = 2 * ra;
@@ -621,18 +630,30 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
   // (the sample index of a row is loaded one tile ahead: sample_j)
   constexpr int TPR = CD_THREADS / CD_ROWS;
   const int grow = threadIdx.x / TPR, gcg = threadIdx.x - grow * TPR;
-  auto sample_j = [&](int tile) { return tile < ntile ? perm[min(g0 + tile * CD_ROWS + grow, g1 - 1)] : 0; };
-  // i0 >= 0: the sample's first-core row, already loaded (site-1 mode)
-  auto issue = [&](int tile, int buf, int j, int i0) {
+  auto sample_j = [&](int tile) {
+    if constexpr (MODE == CD_TAB1) return min(tile * CD_ROWS + grow, g1 - 1);
+    return tile < ntile ? perm[min(g0 + tile * CD_ROWS + grow, g1 - 1)] : 0;
+  };
+  // source row index of sample j (CD_G0: its i_0; CD_TAB2: i_1 n0 + i_0)
+  auto src_index = [&](int j) {
+    if constexpr (MODE == CD_G0) return (long long)idx0[(long long)j * idx_d];
+    if constexpr (MODE == CD_TAB2)
+      return (long long)idx0[(long long)j * idx_d + 1] * n0 + idx0[(long long)j * idx_d];
+    return (long long)j;
+  };
+  // i0 >= 0: the sample's source row, already loaded (gather modes)
+  auto issue = [&](int tile, int buf, int j, long long i0) {
     double* st = buf ? stage1 : stage0;
     int* rj = rowj + buf * CD_ROWS;
     const int t0 = g0 + tile * CD_ROWS;
     const int row = grow, cg = gcg;
-    if (cg == 0) rj[row] = (t0 + row < g1) ? j : -1;
+    if (cg == 0) rj[row] = (t0 + row < g1) ? (MODE == CD_TAB1 ? s * n0 + j : j) : -1;
     const cplx* srow;
-    if constexpr (G0) {
-      if (i0 < 0) i0 = idx0[(long long)j * idx_d];
-      srow = core0 + (long long)i0 * ra;
+    if constexpr (MODE == CD_G0 || MODE == CD_TAB2) {
+      if (i0 < 0) i0 = src_index(j);
+      srow = (MODE == CD_G0 ? core0 : vin) + i0 * ra;
+    } else if constexpr (MODE == CD_TAB1) {
+      srow = core0 + (long long)j * ra;
     } else {
       srow = vin + (long long)j * ra;
     }
@@ -642,7 +663,8 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
     cp_async_commit();
   };
   issue(0, 0, sample_j(0), -1);  // first gather overlaps the slice load below
-  int jnext = sample_j(1), inext = -1;
+  int jnext = sample_j(1);
+  long long inext = -1;
   const cplx* src = cores + inst * stride + offk;
   for (int e = threadIdx.x; e < ra * rb; e += CD_THREADS) {
     const int a = e / rb, c = e - a * rb;
@@ -714,8 +736,8 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
                          : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1]) : "d"(av[mt]), "d"(bv[nt]));
       }
     }
-    if constexpr (G0) {
-      if (tile + 2 < ntile) inext = idx0[(long long)jnext * idx_d];  // jnext has landed by now
+    if constexpr (MODE == CD_G0 || MODE == CD_TAB2) {
+      if (tile + 2 < ntile) inext = src_index(jnext);  // jnext has landed by now
     }
     // c0, c1 = C'[row][2 tig], C'[row][2 tig + 1] = one complex output
 #pragma unroll
@@ -746,7 +768,7 @@ int conv_site_dmma_nt(int rb) {
 cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long offk, int ra, int n,
                                   int rb, const int* perm, const int* goff, const cplx* vin, cplx* vout,
                                   long long vstride, const int* active, int n_inst, cudaStream_t s,
-                                  long long off0, const int* idx0, int idx_d) {
+                                  long long off0, const int* idx0, int idx_d, int mode, int n0) {
   const int nt = conv_site_dmma_nt(rb);
   const size_t smem = conv_site_dmma_smem(ra, rb);
   dim3 grid((unsigned)n, (unsigned)n_inst);
@@ -754,21 +776,20 @@ cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long
   const int ks_need = ((2 * ra + 3) & ~3) / 4;
   const int ks = ks_need <= 4 ? 4 : ks_need <= 8 ? 8 : ks_need <= 16 ? 16 : 0;
   const int code = nt * 100 + ((ks > 0 && ks * nt <= 32) ? ks : 0);
-#define CD_CASE(NT, KS)                                                                          \
-  case NT * 100 + KS: {                                                                          \
-    if (idx0) {                                                                                  \
-      cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS, true>);         \
-      if (e != cudaSuccess) return e;                                                            \
-      conv_site_dmma_kernel<NT, KS, true><<<grid, CD_THREADS, smem, s>>>(                        \
-          cores, stride, offk, ra, n, rb, perm, goff, vin, vout, vstride, active, off0, idx0, idx_d); \
-    } else {                                                                                     \
-      cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS, false>);        \
-      if (e != cudaSuccess) return e;                                                            \
-      conv_site_dmma_kernel<NT, KS, false><<<grid, CD_THREADS, smem, s>>>(                       \
-          cores, stride, offk, ra, n, rb, perm, goff, vin, vout, vstride, active, off0, idx0, idx_d); \
-    }                                                                                            \
-    break;                                                                                       \
+#define CD_LAUNCH(NT, KS, MODE)                                                                  \
+  {                                                                                              \
+    cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS, MODE>);           \
+    if (e != cudaSuccess) return e;                                                              \
+    conv_site_dmma_kernel<NT, KS, MODE><<<grid, CD_THREADS, smem, s>>>(                          \
+        cores, stride, offk, ra, n, rb, perm, goff, vin, vout, vstride, active, off0, idx0, idx_d, n0); \
   }
+#define CD_CASE(NT, KS)                                                                          \
+  case NT * 100 + KS:                                                                            \
+    if (mode == CD_G0) CD_LAUNCH(NT, KS, CD_G0)                                                  \
+    else if (mode == CD_TAB1) CD_LAUNCH(NT, KS, CD_TAB1)                                         \
+    else if (mode == CD_TAB2) CD_LAUNCH(NT, KS, CD_TAB2)                                         \
+    else CD_LAUNCH(NT, KS, CD_PLAIN)                                                             \
+    break;
   switch (code) {
     CD_CASE(1, 0) CD_CASE(1, 4) CD_CASE(1, 8) CD_CASE(1, 16)
     CD_CASE(2, 0) CD_CASE(2, 4) CD_CASE(2, 8) CD_CASE(2, 16)
@@ -777,6 +798,7 @@ cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long
       return cudaErrorInvalidValue;
   }
 #undef CD_CASE
+#undef CD_LAUNCH
   return cudaGetLastError();
 }
 
