@@ -707,7 +707,12 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
     const double* arow = st + (wr * 8 * CD_MT + gid) * KP + tig;
+    // the table's buckets are n0 = N+1 rows (odd): warps whose rows of the
+    // last tile are all past it skip their MMAs (table mode only)
+    bool skip_mma = false;
+    if constexpr (MODE == CD_TAB1) skip_mma = g0 + tile * CD_ROWS + wr * 8 * CD_MT >= g1;
     if constexpr (KS > 0) {
+      if (!skip_mma)
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         if (4 * ks >= Kpad) break;  // KS rounds the k-steps up; columns past Kpad are not staged
