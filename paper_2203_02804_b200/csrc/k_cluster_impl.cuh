@@ -559,7 +559,9 @@ __device__ __forceinline__ cplx vref(const CC& c, int l, int g, int a) {
   return g > a ? Wl(c, l, c.colmap[a]) : mk(g == a ? 1.0 : 0.0, 0.0);
 }
 
-__device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
+// norms: also leave each Q row's squared norm and the starts' initial row
+// positions in vn1/vn2/rpos/rpos2 (the fused starts then skip their norm pass)
+__device__ void form_q_wy(cg::cluster_group& cl, CC& c, bool norms) {
   const int r = c.r, m = c.m, lo = c.row0, nl = c.nrows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   cplx* X = c.aug;          // this CTA's packed partials (read remotely)
@@ -678,6 +680,7 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
   constexpr int OB = 8;
   FOR_MY_ROWS(l, nl, g_serpentine) {  // the Gram pass ran ascending
     const int g = lo + l;
+    double nsq = 0.0, nmx = 0.0;  // sum of squares in column order, largest component
     for (int b0 = 0; b0 < r; b0 += OB) {
       cplx acc[OB];
 #pragma unroll
@@ -715,8 +718,25 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c) {
       }
 #pragma unroll
       for (int q = 0; q < OB; ++q)
-        if (b0 + q < r)
-          c.Qg[(long long)(b0 + q) * m + g] = csub(mk(g == b0 + q ? 1.0 : 0.0, 0.0), acc[q]);
+        if (b0 + q < r) {
+          const cplx qv = csub(mk(g == b0 + q ? 1.0 : 0.0, 0.0), acc[q]);
+          c.Qg[(long long)(b0 + q) * m + g] = qv;
+          nsq = fma(qv.x, qv.x, fma(qv.y, qv.y, nsq));
+          nmx = fmax(nmx, fmax(fabs(qv.x), fabs(qv.y)));
+        }
+    }
+    if (norms) {
+      // plain sum of squares where no scaling is needed; else the scaled
+      // two-pass form over the row just written
+      double n2 = nsq;
+      if (!(nmx == 0.0 || (nmx > 1e-140 && nmx < 1e140))) {
+        __threadfence_block();
+        n2 = ssq_norm2(ssq_of(Qrow(c, g), m, r));
+      }
+      c.vn1[l] = n2;
+      c.vn2[l] = n2;
+      c.rpos[l] = g;
+      c.rpos2[l] = g;
     }
   }
   __threadfence();
@@ -788,7 +808,8 @@ __device__ __forceinline__ cplx warp_transpose_sum16(const cplx* v) {
   return cadd(k1, xch(k1, 1));
 }
 
-__device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank_tol, bool wy, bool fuse_qr) {
+__device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank_tol, bool wy, bool fuse_qr,
+                             bool norms_in_q) {
   const int r = c.r, m = c.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lo = c.row0, nl = c.nrows;
@@ -1147,7 +1168,7 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
   }
   if (lead == 0.0 || mn < rank_tol * lead) return false;
   if (wy) {
-    form_q_wy(cl, c);
+    form_q_wy(cl, c, norms_in_q);
     return true;
   }
   // zung2r: Q = H(0)...H(r-1) [I; 0]
@@ -1663,7 +1684,7 @@ __device__ __forceinline__ void load_qrow_lanes(const CC& c, int g, cplx* dst) {
   __syncwarp();
 }
 
-__device__ void start_pair_s(cg::cluster_group& cl, CC& c, int& par) {
+__device__ void start_pair_s(cg::cluster_group& cl, CC& c, int& par, bool norms_ready) {
   const int r = c.r, lo = c.row0, nl = c.nrows, m = c.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ld = pi_ld(r);
@@ -1681,13 +1702,14 @@ __device__ void start_pair_s(cg::cluster_group& cl, CC& c, int& par) {
     const int cc = e / ld, rr = e - cc * ld;
     Pi[e] = mk((rr == cc) ? 1.0 : 0.0, 0.0);
   }
-  for (int l = threadIdx.x; l < nl; l += CT) {
-    const double n2 = ssq_norm2(ssq_of(Qrow(c, lo + l), m, r));
-    c.vn1[l] = n2;
-    c.vn2[l] = n2;
-    c.rpos[l] = lo + l;
-    c.rpos2[l] = lo + l;
-  }
+  if (!norms_ready)
+    for (int l = threadIdx.x; l < nl; l += CT) {
+      const double n2 = ssq_norm2(ssq_of(Qrow(c, lo + l), m, r));
+      c.vn1[l] = n2;
+      c.vn2[l] = n2;
+      c.rpos[l] = lo + l;
+      c.rpos2[l] = lo + l;
+    }
   int f0 = lane, f1 = lane + 32;  // warp 0: QRCP first[]; warp 1: LU first[]
   __syncthreads();
   for (int k = 0; k < r; ++k) {
@@ -2164,7 +2186,9 @@ __global__ void __launch_bounds__(CT, CLUSTER_MIN_BLOCKS) cluster_bond_kernel(Cl
   PHASE_MARK(0);
   load_block(c, J, inst);
   PHASE_MARK(1);
-  if (!column_basis(cl, c, par, job.rank_tol, J.q_wy != 0, J.fused_qr != 0)) {
+  // the WY Q pass also leaves the fused starts' row norms (m > r only)
+  const bool norms_in_q = J.q_wy != 0 && J.fused_starts != 0 && job.m != job.r;
+  if (!column_basis(cl, c, par, job.rank_tol, J.q_wy != 0, J.fused_qr != 0, norms_in_q)) {
     if (c.crank == 0 && threadIdx.x == 0) set_error(job, inst, TTP_ERR_SINGULAR);
     cl.sync();
     return;
@@ -2176,7 +2200,7 @@ __global__ void __launch_bounds__(CT, CLUSTER_MIN_BLOCKS) cluster_bond_kernel(Cl
   } else {
     PHASE_MARK(2);
     if (J.fused_starts) {
-      start_pair_s(cl, c, par);
+      start_pair_s(cl, c, par, norms_in_q);
       PHASE_MARK(3);
     } else {
       start_qrcp_qh_s(cl, c, par);
