@@ -91,6 +91,7 @@ constexpr int QX_ROWS = QX_ROWS_DEF;  // rows per staged tile of the DMMA Q*X pr
 constexpr int LAZY_MAX = 4;  // most deferred swap updates (global-slice mode)
 __constant__ int g_lazy_f = LAZY_MAX;  // flush cadence of the deferred updates (1 = eager)
 __constant__ int g_serpentine = 1;  // dev knob (A/B of the serpentine row order)
+__constant__ int g_gram_dmma = 1;   // WY Gram on DMMA (else the 4x4 scalar tiles)
 
 struct __align__(16) Rec {
   double v;
@@ -559,6 +560,112 @@ __device__ __forceinline__ cplx vref(const CC& c, int l, int g, int a) {
   return g > a ? Wl(c, l, c.colmap[a]) : mk(g == a ? 1.0 : 0.0, 0.0);
 }
 
+// Gram partials X[a r + b] = sum_{local rows g >= r} conj(V(g,a)) V(g,b),
+// a < b, on the FP64 tensor cores (r <= 32, qtile present): the rows stream
+// through the Q*X staging tiles by cp.async (double-buffered, V columns in
+// logical order, real interleaved) and the real Gram of the interleaved
+// rows accumulates in DMMA fragments (each warp owns upper-triangle 8x8
+// tiles); the complex entries follow from its 2x2 blocks.  Every V element
+// is read from global memory once.
+__device__ void gram_dmma(const CC& c, cplx* X) {
+  const int r = c.r, nl = c.nrows, lo = c.row0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int Kp = (2 * r + 3) & ~3, ldA = Kp + 4;
+  const int nt8 = (2 * r + 7) / 8;              // real 8-wide tiles per side
+  const int ntiles = nt8 * (nt8 + 1) / 2;       // upper triangle incl. diagonal
+  constexpr int MAXT = 8;                       // tiles per warp (36 / CW)
+  double acc[MAXT][2];
+#pragma unroll
+  for (int q = 0; q < MAXT; ++q) acc[q][0] = acc[q][1] = 0.0;
+  double* tiles[2] = {c.qtile, c.qtile + QX_ROWS * ldA};
+  __syncthreads();  // the region is shared with the starts' per-row state
+  for (int e = threadIdx.x; e < 2 * QX_ROWS * (Kp - 2 * r); e += CT) {
+    const int bb = e / (QX_ROWS * (Kp - 2 * r)), e2 = e - bb * QX_ROWS * (Kp - 2 * r);
+    const int row = e2 / (Kp - 2 * r), k = 2 * r + (e2 - row * (Kp - 2 * r));
+    tiles[bb][row * ldA + k] = 0.0;
+  }
+  const int lfast = max(0, r - lo);  // rows below hold the unit-diagonal part of V
+  // rows past nl are zero-filled by cp.async with a 0-byte source
+  auto issue = [&](int l0, double* dst) {
+    for (int e = threadIdx.x; e < QX_ROWS * r; e += CT) {
+      const int t = e / QX_ROWS, row = e - t * QX_ROWS;
+      const int l = l0 + row;
+      const cplx* src = c.Ws + (long long)c.colmap[t] * c.ldw + min(l, nl - 1);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + row * ldA + 2 * t);
+      const int bytes = (l < nl) ? 16 : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(bytes));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  if (lfast < nl) issue(lfast, tiles[0]);
+  int buf = 0;
+  for (int l0 = lfast; l0 < nl; l0 += QX_ROWS, buf ^= 1) {
+    if (l0 + QX_ROWS < nl) {
+      issue(l0 + QX_ROWS, tiles[buf ^ 1]);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* tile = tiles[buf];
+#pragma unroll
+    for (int q = 0; q < MAXT; ++q) {
+      const int tt = warp + q * CW;
+      if (tt < ntiles) {
+        int ti = 0, rem = tt;
+        while (rem >= nt8 - ti) {
+          rem -= nt8 - ti;
+          ++ti;
+        }
+        const int tj = ti + rem;
+        // A(m, k) = tile[k][ti*8 + m], B(k, n) = tile[k][tj*8 + n]
+#pragma unroll
+        for (int k0 = 0; k0 < QX_ROWS; k0 += 4) {
+          const double av = tile[(k0 + tig) * ldA + ti * 8 + gid];
+          const double bv = tile[(k0 + tig) * ldA + tj * 8 + gid];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[q][0]), "+d"(acc[q][1]) : "d"(av), "d"(bv));
+        }
+      }
+    }
+    __syncthreads();  // tile buf is refilled by the issue two steps later
+  }
+  // complex entries from the real 2x2 blocks: lane (gid = 2p, tig) holds
+  // R(2a, 2b), R(2a, 2b+1); its partner gid = 2p + 1 (lane ^ 4) holds
+  // R(2a+1, 2b), R(2a+1, 2b+1), with a = 4 ti + p, b = 4 tj + tig
+#pragma unroll
+  for (int q = 0; q < MAXT; ++q) {
+    const int tt = warp + q * CW;
+    if (tt < ntiles) {
+      int ti = 0, rem = tt;
+      while (rem >= nt8 - ti) {
+        rem -= nt8 - ti;
+        ++ti;
+      }
+      const int tj = ti + rem;
+      const double o0 = __shfl_xor_sync(0xffffffffu, acc[q][0], 4);
+      const double o1 = __shfl_xor_sync(0xffffffffu, acc[q][1], 4);
+      if ((gid & 1) == 0) {
+        const int a = 4 * ti + (gid >> 1), b = 4 * tj + tig;
+        if (a < b && b < r) X[a * r + b] = mk(acc[q][0] + o1, acc[q][1] - o0);
+      }
+    }
+  }
+  // the unit-diagonal rows (g < r, CTA 0 only): V(g,a) = 1 (g == a), W (g > a), 0
+  if (lfast > 0) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < r * r; e += CT) {
+      const int a = e / r, b = e - a * r;
+      if (a < b) {
+        cplx s = X[e];
+        for (int l = 0; l < min(lfast, nl); ++l) s = cfmac(vref(c, l, lo + l, a), vref(c, l, lo + l, b), s);
+        X[e] = s;
+      }
+    }
+  }
+}
+
 // norms: also leave each Q row's squared norm and the starts' initial row
 // positions in vn1/vn2/rpos/rpos2 (the fused starts then skip their norm pass)
 __device__ void form_q_wy(cg::cluster_group& cl, CC& c, bool norms) {
@@ -568,8 +675,12 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c, bool norms) {
   cplx* P = c.aug + r * r;  // reduced: strict upper = V^H V, strict lower = V1
   cplx* T = c.selb;         // r x r row-major, upper triangular
   SP_BEGIN(spw);
-  // (1) Gram partials over local rows, 4 x 4 tiles (upper tile triangle),
-  //     lanes stride rows (coalesced column reads), one warp per tile.
+  // (1) Gram partials over local rows: on DMMA when the staging tile exists
+  //     (r <= 32), else 4 x 4 tiles (upper tile triangle), lanes stride rows
+  //     (coalesced column reads), one warp per tile.
+  if (c.qtile && g_gram_dmma) {
+    gram_dmma(c, X);
+  } else {
   constexpr int TB = 4;
   const int nt = (r + TB - 1) / TB;
   const int ntiles = nt * (nt + 1) / 2;
@@ -623,6 +734,7 @@ __device__ void form_q_wy(cg::cluster_group& cl, CC& c, bool norms) {
         const int a = a0 + u, b = b0 + v;
         if (lane == 0 && a < b && b < r) X[a * r + b] = s;
       }
+  }
   }
   // strict lower: V1(a, b), a > b, from the CTA owning row a (0 elsewhere)
   for (int e = threadIdx.x; e < r * r; e += CT) {
