@@ -91,6 +91,7 @@ constexpr int QX_ROWS = QX_ROWS_DEF;  // rows per staged tile of the DMMA Q*X pr
 constexpr int LAZY_MAX = 4;  // most deferred swap updates (global-slice mode)
 __constant__ int g_lazy_f = LAZY_MAX;  // flush cadence of the deferred updates (1 = eager)
 __constant__ int g_serpentine = 1;  // dev knob (A/B of the serpentine row order)
+__constant__ int g_swap_filter = 1;  // bound-filtered swap passes (global-slice mode); A/B knob
 __constant__ int g_gram_dmma = 1;   // WY Gram on DMMA (else the 4x4 scalar tiles)
 
 struct __align__(16) Rec {
@@ -2030,7 +2031,9 @@ __device__ __forceinline__ void cluster_wait() {
 // the eager updates would have run, so every value (and the argmax) is
 // bitwise the eager one.  flush: write the current B back (B_W := B).
 // Returns my best |B|^2 candidate.
-template <int NP>
+// BND: also leave each row's max |B(l, t)| in c.vn1 (the exact bound the
+// filtered passes below start from; vn1 is free once the starts are done).
+template <int NP, bool BND>
 __device__ __forceinline__ Cand swap_pass(const CC& c, const cplx* pw, const int* pj, bool flush, bool rev) {
   const int r = c.r, lo = c.row0, nl = c.nrows;
   // running best as (|v|^2, 32-bit row-major key): fewer live registers
@@ -2048,6 +2051,7 @@ __device__ __forceinline__ Cand swap_pass(const CC& c, const cplx* pw, const int
 #pragma unroll
       for (int u = 0; u < s; ++u) cs[s] = cfma(cs[u], pw[u * r + pj[s]], cs[s]);
     const int rk = (lo + l) * r;
+    double rm = 0.0;
     int t = 0;
     // the hottest loop: 16 loads in flight (8 with three or more pending
     // updates, whose coefficients take the registers)
@@ -2066,6 +2070,7 @@ __device__ __forceinline__ Cand swap_pass(const CC& c, const cplx* pw, const int
         for (int s = 0; s < NP; ++s) v = cfma(cs[s], pw[s * r + t + q], v);
         if (flush) p[(t + q) * ld] = v;
         const double v2 = cabs2(v);
+        if (BND) rm = fmax(rm, v2);
         if (v2 > bv || (v2 == bv && rk + t + q < bk)) {
           bv = v2;
           bk = rk + t + q;
@@ -2078,11 +2083,114 @@ __device__ __forceinline__ Cand swap_pass(const CC& c, const cplx* pw, const int
       for (int s = 0; s < NP; ++s) v = cfma(cs[s], pw[s * r + t], v);
       if (flush) p[t * ld] = v;
       const double v2 = cabs2(v);
+      if (BND) rm = fmax(rm, v2);
       if (v2 > bv || (v2 == bv && rk + t < bk)) {
         bv = v2;
         bk = rk + t;
       }
     }
+    if (BND) c.vn1[l] = sqrt(rm);
+  }
+  Cand a{-1.0, LLONG_MAX, -1};
+  if (bk != INT_MAX) a = Cand{bv, (long long)bk, bk / r - lo};
+  return a;
+}
+
+// Bound-filtered row pass (global-slice mode, no flush).  c.vn1[l] holds an
+// upper bound on max_t |B(l, t)|; the newest update B += c_n(l) w_n raises it
+// by at most |c_n(l)| max_t |w_n[t]|.  T is a running lower bound on the
+// warp's maximum: the warp's best entry of the previous pass, re-evaluated,
+// then every exact entry this pass has formed so far.  A row first forms its
+// update coefficients (NP column loads, as in swap_pass) and its entry in the
+// newest pivot column; only if its bound reaches T (with a 1e-11 relative
+// margin over the rounding of the bounds) are its other entries read.  Every
+// skipped row's entries are below T, and every evaluated entry runs the same
+// fma chain as swap_pass, so the warp's best (value, row-major key) is
+// bitwise the one the full pass returns.  A row costs the full pass's loads
+// at worst (the cluster barrier waits for the slowest warp), and one
+// coalesced load per pending update when skipped.
+template <int NP>
+__device__ __forceinline__ Cand swap_pass_filt(const CC& c, const cplx* pw, const int* pj, double wmax,
+                                               const Cand prev, bool rev) {
+  const int r = c.r, lo = c.row0, nl = c.nrows;
+  const long long ld = c.ldw;
+  const int jn = pj[NP - 1];
+  const cplx wnj = pw[(NP - 1) * r + jn];
+  double* bnd = c.vn1;
+  double bv = -1.0;
+  int bk = INT_MAX;
+  auto take = [&](double v2, int key) {
+    if (v2 > bv || (v2 == bv && key < bk)) {
+      bv = v2;
+      bk = key;
+    }
+  };
+  // chain of the row's update coefficients (same fma order as swap_pass)
+  auto coeffs = [&](const cplx* p, cplx* cs) {
+#pragma unroll
+    for (int s = 0; s < NP; ++s) cs[s] = p[pj[s] * ld];
+#pragma unroll
+    for (int s = 1; s < NP; ++s)
+#pragma unroll
+      for (int u = 0; u < s; ++u) cs[s] = cfma(cs[u], pw[u * r + pj[s]], cs[s]);
+  };
+  const int prow = prev.row;  // the warp's previous best (local row), or -1
+  if (prow >= 0 && prow % CT == (int)threadIdx.x) {
+    const int pt = (int)(prev.key - (long long)(lo + prow) * r);
+    const cplx* p = c.Ws + prow;
+    cplx cs[NP];
+    coeffs(p, cs);
+    cplx v = p[pt * ld];
+#pragma unroll
+    for (int s = 0; s < NP; ++s) v = cfma(cs[s], pw[s * r + pt], v);
+    take(cabs2(v), (lo + prow) * r + pt);
+  }
+  double T2 = bv;
+  const int nk = (nl + CT - 1) / CT;
+  constexpr int KS = NP <= 2 ? 2 * KB : KB;
+  for (int k = 0; k < nk; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) T2 = fmax(T2, __shfl_xor_sync(0xffffffffu, T2, o));
+    const int l = (int)threadIdx.x + (rev ? nk - 1 - k : k) * CT;
+    if (l < nl) {
+      const cplx* p = c.Ws + l;
+      cplx cs[NP];
+      coeffs(p, cs);
+      const double bo = bnd[l];
+      const cplx cn = cs[NP - 1];
+      const int rk = (lo + l) * r;
+      take(cabs2(cfma(cn, wnj, cn)), rk + jn);  // entry (l, jn) after the update
+      double bound = fma(sqrt(cabs2(cn)), wmax, bo);
+      if (!(bound * bound < T2 * (1.0 - 1e-11))) {
+        double rm = 0.0;
+        int t = 0;
+        for (; t + KS <= r; t += KS) {
+          cplx x[KS];
+#pragma unroll
+          for (int q = 0; q < KS; ++q) x[q] = p[(t + q) * ld];
+#pragma unroll
+          for (int q = 0; q < KS; ++q) {
+            cplx v = x[q];
+#pragma unroll
+            for (int s = 0; s < NP; ++s) v = cfma(cs[s], pw[s * r + t + q], v);
+            const double v2 = cabs2(v);
+            rm = fmax(rm, v2);
+            take(v2, rk + t + q);
+          }
+        }
+        for (; t < r; ++t) {
+          cplx v = p[t * ld];
+#pragma unroll
+          for (int s = 0; s < NP; ++s) v = cfma(cs[s], pw[s * r + t], v);
+          const double v2 = cabs2(v);
+          rm = fmax(rm, v2);
+          take(v2, rk + t);
+        }
+        bound = sqrt(rm);
+      }
+      bnd[l] = bound;
+    }
+    T2 = fmax(T2, bv);
   }
   Cand a{-1.0, LLONG_MAX, -1};
   if (bk != INT_MAX) a = Cand{bv, (long long)bk, bk / r - lo};
@@ -2102,6 +2210,8 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
   int* pj = lazy ? c.pendj : c.ibc + 8;  // pending j_s
   const int F = lazy ? max(1, min(LAZY_MAX, g_lazy_f)) : 1;
   int np = 0;  // updates not yet written to the slice
+  const bool filter = lazy && g_swap_filter;
+  bool bvalid = false;  // c.vn1 holds row bounds of the current B
   // global-slice mode: peers read winner rows straight from my slice, so no
   // CTA may rewrite its slice (form_B, a flushing pass) while a peer can
   // still be reading the previous winner row from it
@@ -2112,6 +2222,7 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
   SP_BEGIN(spt);
   for (long long it = 0;; ++it) {
     a = warp_cand(a);
+    const Cand wb = a;  // this warp's best entry (the filtered pass re-evaluates it)
     __syncwarp();
     if (c.ns_global) {
       // global-slice mode: the winner's row is read straight from its
@@ -2161,6 +2272,15 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
           w[lane + 32] = cdiv(csub(c.selb[j * r + lane + 32], x1), pivot);
         }
         if (lane == 0) pj[np] = j;
+        if (filter) {
+          // max_t |w[t]| for the filtered passes' bounds, rounded up
+          double wm = 0.0;
+          if (lane < r) wm = cabsh(w[lane]);
+          if (lane + 32 < r) wm = fmax(wm, cabsh(w[lane + 32]));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) wm = fmax(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+          if (lane == 0) c.dbc[6] = wm * (1.0 + 1e-12);
+        }
       }
       if (lane == 0) {
         c.ibc[4] = i;
@@ -2201,11 +2321,24 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
     if (fence) cluster_wait();
     SP(spt, 12);
     const bool rev = g_serpentine && ((it & 1) == 0);
-    switch (nq) {
-      case 1: a = swap_pass<1>(c, pw, pj, flush, rev); break;
-      case 2: a = swap_pass<2>(c, pw, pj, flush, rev); break;
-      case 3: a = swap_pass<3>(c, pw, pj, flush, rev); break;
-      default: a = swap_pass<4>(c, pw, pj, flush, rev); break;
+    if (filter && bvalid && !flush) {
+      const double wmax = c.dbc[6];
+      switch (nq) {
+        case 1: a = swap_pass_filt<1>(c, pw, pj, wmax, wb, rev); break;
+        case 2: a = swap_pass_filt<2>(c, pw, pj, wmax, wb, rev); break;
+        case 3: a = swap_pass_filt<3>(c, pw, pj, wmax, wb, rev); break;
+        default: a = swap_pass_filt<4>(c, pw, pj, wmax, wb, rev); break;
+      }
+    } else {
+      // full pass; its row bounds are only used in global-slice mode (vn1 is
+      // free during the swaps in every mode)
+      switch (nq) {
+        case 1: a = swap_pass<1, true>(c, pw, pj, flush, rev); break;
+        case 2: a = swap_pass<2, true>(c, pw, pj, flush, rev); break;
+        case 3: a = swap_pass<3, true>(c, pw, pj, flush, rev); break;
+        default: a = swap_pass<4, true>(c, pw, pj, flush, rev); break;
+      }
+      bvalid = filter;
     }
     np = flush ? 0 : nq;
     SP(spt, 13);
@@ -2214,6 +2347,7 @@ __device__ int swap_to_dominance_s(cg::cluster_group& cl, CC& c, int& par, doubl
       invert_rows(c, c.sel);
       a = form_B(c);
       np = 0;
+      bvalid = false;
     }
   }
   par ^= 1;
@@ -2564,6 +2698,18 @@ static cudaError_t apply_lazy_knob() {
   return st;
 }
 
+// TTP_SWAP_FILTER=0 runs every deferred swap pass over all rows (A/B knob);
+// default: bound-filtered passes between the flushing ones.
+static cudaError_t apply_swap_filter_knob() {
+  static const cudaError_t st = [] {
+    const char* e = getenv("TTP_SWAP_FILTER");
+    if (!e) return cudaSuccess;
+    const int f = e[0] == '0' ? 0 : 1;
+    return cudaMemcpyToSymbol(g_swap_filter, &f, sizeof(int));
+  }();
+  return st;
+}
+
 // TTP_FUSED_QR=0 runs the column basis with a separate partials pass per
 // step (A/B knob); default: each update pass also produces the next step's
 // partials.
@@ -2579,7 +2725,8 @@ cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream
   ClusterJob job = job_in;
   job.fused_qr = fused_qr_enabled() ? 1 : 0;
   {
-    const cudaError_t e = apply_lazy_knob();
+    cudaError_t e = apply_lazy_knob();
+    if (e == cudaSuccess) e = apply_swap_filter_knob();
     if (e != cudaSuccess) return e;
   }
   resolve_big(job);
