@@ -476,6 +476,30 @@ def test_throughput_and_latency_cluster_kernels_agree(tmp_path):
         np.testing.assert_array_equal(out["tp"][k], out["lat"][k])
 
 
+def test_swap_filter_is_bitwise_neutral(tmp_path):
+    """The bound-filtered swap passes (global-slice mode) skip rows whose
+    bound on max|B| stays below the warp's running best; the swap sequence,
+    and so every core of a cfg4 batch of 17, is bitwise the one of the
+    unfiltered passes (TTP_SWAP_FILTER=0), on both kernel instantiations."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "sf.py"
+    script.write_text(_CK_SCRIPT)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for ck in ("tp", "lat"):
+        out = {}
+        for f in ("0", "1"):
+            env = dict(os.environ, TTP_CK=ck, TTP_SWAP_FILTER=f)
+            path = tmp_path / f"{ck}{f}.npz"
+            subprocess.run([sys.executable, str(script), str(path)], check=True, env=env, cwd=root,
+                           timeout=600)
+            out[f] = np.load(path)
+        assert len(out["0"].files) == len(out["1"].files) > 0
+        for k in out["0"].files:
+            np.testing.assert_array_equal(out["0"][k], out["1"][k])
+
+
 def test_throughput_kernel_batch_composition_and_properties():
     """Batches above 16 take the throughput instantiation: an instance's
     cores do not depend on its batch neighbours or position, repeated runs
