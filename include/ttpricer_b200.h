@@ -163,10 +163,6 @@ void ttp_profile_enable(int on);
 void ttp_profile_reset(void);
 int ttp_profile_read(ttp_kernel_stat* out, int32_t max_entries);
 
-/* Diagnostics: clock64() phase marks of the cluster bond kernel for instance 0
- * (enable != 0 arms them; out receives up to n marks of the last launch). */
-int ttp_debug_phase_clocks(int enable, int64_t* out, int32_t n);
-
 /* K1/K2 fiber evaluators at explicit multi-indices (shared by all
  * instances): d_out[i*m + j] = oracle_i(d_idx[j, :]).
  * Replaces phi_grid_oracle / payoff_grid_oracle calls (pricers.py:234-253). */

@@ -23,7 +23,12 @@ from .errors import (
 )
 
 LIB_NAME = "libttpricer_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# The dev variant (`make -C csrc dev`, -DTTP_DEV) carries the TTP_* A/B knobs;
+# it is loaded only when TTP_DEV_LIBRARY=1 (tools/ and the knob-neutrality
+# tests, each in its own process).  Everything else runs the release library.
+DEV_LIB_NAME = "libttpricer_b200_dev.so"
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, DEV_LIB_NAME if os.environ.get("TTP_DEV_LIBRARY") == "1" else LIB_NAME)
 
 TTP_OK = 0
 TTP_ERR_INVALID = 1
@@ -153,7 +158,6 @@ SIGNATURES = [
     ("ttp_profile_enable", None, [ctypes.c_int]),
     ("ttp_profile_reset", None, []),
     ("ttp_profile_read", _i32, [ctypes.POINTER(KernelStat), _i32]),
-    ("ttp_debug_phase_clocks", _i32, [ctypes.c_int, ctypes.POINTER(_i64), _i32]),
     ("ttp_oracle_eval", _i32, [ctypes.POINTER(Oracle), _p, _i32, _p, _i64, _p, _p]),
     ("ttp_tt_inner", _i32, [ctypes.POINTER(TTBatch), ctypes.POINTER(TTBatch), _p, _p]),
     ("ttp_tt_eval_workspace", _sz, [ctypes.POINTER(TTBatch), _i64]),
@@ -194,14 +198,17 @@ def load_library(path=LIB_PATH):
             return _lib
         if not os.path.exists(path):
             raise DeviceError(
-                f"{LIB_NAME} is not built (expected at {path}); run "
-                "`make -C paper_2203_02804_b200/csrc` or __graft_entry__.build()"
+                f"{os.path.basename(path)} is not built (expected at {path}); run "
+                "`make -C paper_2203_02804_b200/csrc` (or `... dev`) or __graft_entry__.build()"
             )
         lib = ctypes.CDLL(path)
         for name, res, args in SIGNATURES:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if hasattr(lib, "ttp_dev_phase_clocks"):  # dev build only
+            lib.ttp_dev_phase_clocks.restype = _i32
+            lib.ttp_dev_phase_clocks.argtypes = [ctypes.c_int, ctypes.POINTER(_i64), _i32]
         if lib.ttp_abi_version() != 1:
             raise DeviceError("libttpricer_b200.so ABI version mismatch")
         _lib = lib

@@ -196,7 +196,9 @@ class _ConvSamples:
 
     @classmethod
     def get(cls, shape, m, seed):
-        key = (tuple(shape), int(m), seed)
+        # the tensors live on the device that was current when they were made
+        torch = _lib.require_device()
+        key = (tuple(shape), int(m), seed, torch.cuda.current_device())
         if key not in cls._cache:
             if len(cls._cache) > 8:
                 cls._cache.clear()

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "ttp_internal.h"
+#include "dev_knobs.h"
 #include "launch.h"
 #include "k_bond.h"
 
@@ -35,10 +36,10 @@ cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long
                                   long long off0 = 0, const int* idx0 = nullptr, int idx_d = 0,
                                   int mode = 0, int n0 = 0);
 
-// TTP_CONV_DMMA=0 selects the scalar-FMA site kernel (A/B checks).
+// TTP_CONV_DMMA=0 selects the scalar-FMA site kernel (dev build A/B checks).
 bool conv_dmma_enabled() {
   static const bool on = [] {
-    const char* e = getenv("TTP_CONV_DMMA");
+    const char* e = ttp_dev_env("TTP_CONV_DMMA");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -200,16 +201,22 @@ SetView set_view(const int* base, const ttp_cross_layout& L, int k, int d) {
   return v;
 }
 
-// TTP_BOND_PATH=v0 forces the one-CTA-per-instance global-memory kernel
-// (k_bond_v0.cu); default is the cluster kernel whenever the block fits in
-// the cluster's distributed shared memory.
-// TTP_BOND_PATH: "v0" / "cluster" force a path; default "auto" picks the
-// cluster kernel when the batch fits in about two waves of clusters (latency
-// bound regime) and the one-CTA-per-instance kernel for large batches, where
-// occupying every SM wins.
+// Bond path selection.  The release library picks the path from the block
+// shape alone, never from the batch size, so an option's cores and price do
+// not depend on how many other options share its launch (the reference's
+// determinism contracts, test_cross.py:180-190 and test_bench_cli.py:151-158):
+//   * blocks of >= 1 MB (cfg4, cfg5): global-slice clusters of 2 CTAs, the
+//     256-thread two-CTAs-per-SM instantiation (ck_tp) when its carve fits
+//     twice per SM (r <= 32), else the 512-thread one (ck_lat, r = 64);
+//   * smaller blocks (cfg1-3, the reference test suite): the one-CTA-per-
+//     instance kernel (k_bond_v0.cu) after the fiber kernel.
+// Measured on B200 (profiles/r01/path_sweep*.log): at throughput batch sizes
+// these are the fastest paths for their block sizes.  Dev builds keep the
+// other paths reachable for A/B runs: TTP_BOND_PATH=v0 | cluster (shared-
+// memory clusters) | l2:C (global-slice clusters of C CTAs), TTP_CK=lat|tp.
 int bond_path_mode() {
   static const int v = [] {
-    const char* e = getenv("TTP_BOND_PATH");
+    const char* e = ttp_dev_env("TTP_BOND_PATH");
     if (e && std::strcmp(e, "v0") == 0) return 1;
     if (e && std::strcmp(e, "cluster") == 0) return 2;
     if (e && std::strncmp(e, "l2", 2) == 0) return 3;
@@ -218,67 +225,60 @@ int bond_path_mode() {
   return v;
 }
 
-// Cluster size of the global-slice ("l2") mode: TTP_BOND_PATH=l2:C.
+// Cluster size of the global-slice mode (dev: TTP_BOND_PATH=l2:C); powers of
+// two only, since the row split assumes it (3-CTA clusters fault).
 int l2_cluster_size() {
   static const int v = [] {
-    const char* e = getenv("TTP_BOND_PATH");
-    // powers of two only (the row split assumes it; 3-CTA clusters fault)
-    int c = (e && std::strncmp(e, "l2:", 3) == 0) ? std::max(1, atoi(e + 3)) : 8;
+    const char* e = ttp_dev_env("TTP_BOND_PATH");
+    int c = (e && std::strncmp(e, "l2:", 3) == 0) ? std::max(1, atoi(e + 3)) : 2;
     int p = 1;
     while (p * 2 <= std::min(c, 16)) p *= 2;
     return p;
   }();
   return v;
 }
-bool force_v0() { return bond_path_mode() == 1; }
 
-// Global-slice clusters: the 256-thread, two-CTAs-per-SM instantiation
-// (ck_tp) for throughput batches, the 512-thread one (ck_lat) when a few
-// instances leave SMs idle anyway.  TTP_CK=lat|tp forces one (A/B knob).
+// dev: TTP_CK=lat|tp forces a global-slice instantiation
 static int tp_knob() {
   static const int forced = [] {
-    const char* e = getenv("TTP_CK");
+    const char* e = ttp_dev_env("TTP_CK");
     if (e && std::strcmp(e, "lat") == 0) return 0;
     if (e && std::strcmp(e, "tp") == 0) return 1;
     return -1;
   }();
   return forced;
 }
-bool tp_forced() { return tp_knob() == 1; }
-bool use_tp_kernel(int n) { return tp_knob() >= 0 ? tp_knob() == 1 : n > 16; }
 
 size_t smem_optin_limit() {
-  static size_t lim = [] {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, size_t> memo;
+  return ttp_device_memo(memo, mu, 0, [] {
     int dev = 0, v = 0;
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 0;
     return (size_t)v;
-  }();
-  return lim;
+  });
+}
+
+// Largest power of two <= min(want, m / r): every CTA of a cluster must own
+// at least r rows, and the row split assumes a power of two.
+int pow2_cluster(int want, int m, int r) {
+  const int cap = std::max(1, std::min(want, m / std::max(1, r)));
+  int p = 1;
+  while (p * 2 <= cap) p *= 2;
+  return p;
 }
 
 // One bond for every active instance: fibers + column basis + maxvol +
-// factor.  Cluster kernel (fibers evaluated in shared memory) when the block
-// fits, otherwise the fiber kernel followed by the global-memory bond kernel.
+// factor (path chosen from the block shape, see above).
 int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const CrossWs& w, int n,
              cudaStream_t s) {
-  // Measured on B200 (profiles/r01/path_sweep.log, path_sweep2.log): for
-  // blocks of >= 1 MB (cfg4/cfg5) at throughput batch sizes, clusters of 2
-  // CTAs with the row slices L2-resident beat the one-CTA kernel and 16-CTA
-  // shared-memory clusters (more instances in flight per barrier round);
-  // smaller blocks run fastest on the one-CTA kernel.
   const long long block_bytes = (long long)bj.m * bj.r * (long long)sizeof(cplx);
-  // small batches of blocks too large for a shared-memory cluster (r = 64,
-  // cfg5) also take the global-slice kernel, with more CTAs per instance
-  const bool smem_fits = !force_v0() && ck_lat::pick_cluster_size(bj.m, bj.r, smem_optin_limit()) > 0;
-  const bool auto_l2 = bond_path_mode() == 0 && block_bytes >= (1LL << 20) && (n > 16 || !smem_fits);
-  if (bond_path_mode() == 3 || auto_l2) {
+  const int mode = bond_path_mode();
+  if (mode == 3 || (mode == 0 && block_bytes >= (1LL << 20))) {
     ClusterJob cj{};
     cj.b = bj;
-    int small_c = 2;
-    while (small_c < 16 && n * small_c * 2 <= 148) small_c *= 2;
-    const int want = bond_path_mode() == 3 ? l2_cluster_size() : (n > 16 ? 2 : small_c);
-    cj.cl = std::min(want, std::max(1, bj.m / std::max(1, bj.r)));
+    cj.cl = pow2_cluster(l2_cluster_size(), bj.m, bj.r);
     cj.src_mode = 0;
     cj.fiber_fast = fiber_fast_enabled() ? 1 : 0;
     cj.oracle = o;
@@ -288,20 +288,19 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
     cj.Wg = w.W;
     cj.Sg = w.B;
     cj.wg_stride = w.mat_stride;
-    // throughput batches take the two-CTAs-per-SM instantiation when its
-    // carve fits twice per SM (r <= 32); r = 64 stays on 512-thread CTAs
-    if (use_tp_kernel(n) && (tp_forced() || ck_tp::max_active_clusters(cj) > ck_lat::max_active_clusters(cj))) {
-      if (ck_tp::max_active_clusters(cj) > 0) {
-        TTP_CUDA_CHECK(ck_tp::launch_cluster_bond(cj, n, s));
-        return TTP_OK;
-      }
-    } else if (ck_lat::max_active_clusters(cj) > 0) {
+    const int act_tp = ck_tp::max_active_clusters(cj), act_lat = ck_lat::max_active_clusters(cj);
+    const bool tp = tp_knob() >= 0 ? tp_knob() == 1 : act_tp > act_lat;
+    if (tp && act_tp > 0) {
+      TTP_CUDA_CHECK(ck_tp::launch_cluster_bond(cj, n, s));
+      return TTP_OK;
+    }
+    if (!tp && act_lat > 0) {
       TTP_CUDA_CHECK(ck_lat::launch_cluster_bond(cj, n, s));
       return TTP_OK;
     }
   }
-  const int C = force_v0() ? 0 : ck_lat::pick_cluster_size(bj.m, bj.r, smem_optin_limit());
-  if (C > 0) {
+  if (mode == 2) {
+    const int C = ck_lat::pick_cluster_size(bj.m, bj.r, smem_optin_limit());
     ClusterJob cj{};
     cj.b = bj;
     cj.cl = C;
@@ -311,9 +310,7 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
     cj.fiber = f;
     cj.Qg = w.A;
     cj.q_stride = w.mat_stride;
-    const int act = ck_lat::max_active_clusters(cj);
-    const bool use = act > 0 && (bond_path_mode() == 2 || n <= 2 * act);
-    if (use) {
+    if (C > 0 && ck_lat::max_active_clusters(cj) > 0) {
       TTP_CUDA_CHECK(ck_lat::launch_cluster_bond(cj, n, s));
       return TTP_OK;
     }
@@ -662,7 +659,7 @@ extern "C" int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const doubl
   bj.sel_stride = cols;
   bj.write_mode = 0;
   TTP_CUDA_CHECK(cudaMemsetAsync(bj.status, 0, sizeof(int) * n_mat, s));
-  const int C = force_v0() ? 0 : ck_lat::pick_cluster_size((int)rows, cols, smem_optin_limit());
+  const int C = bond_path_mode() == 1 ? 0 : ck_lat::pick_cluster_size((int)rows, cols, smem_optin_limit());
   ClusterJob cj{};
   cj.b = bj;
   cj.cl = C;
@@ -751,9 +748,10 @@ extern "C" int ttp_price_tt_batch(const ttp_price_problem* prob, ttp_cross_out* 
   return TTP_OK;
 }
 
+#ifdef TTP_DEV
 // Phase clocks of whichever cluster instantiation ran since the last enable
-// (dev tool tools/phase_timing.py).
-extern "C" int ttp_debug_phase_clocks(int enable, int64_t* out, int32_t n) {
+// (dev build only; tools/phase_timing.py).
+extern "C" int ttp_dev_phase_clocks(int enable, int64_t* out, int32_t n) {
   int64_t a[32] = {}, b[32] = {};
   int st = ck_tp::debug_phase_clocks(0, a, 32);
   if (st == TTP_OK) st = ck_lat::debug_phase_clocks(0, b, 32);
@@ -766,3 +764,4 @@ extern "C" int ttp_debug_phase_clocks(int enable, int64_t* out, int32_t n) {
   if (st == TTP_OK) st = ck_lat::debug_phase_clocks(enable, nullptr, 0);
   return st;
 }
+#endif

@@ -62,7 +62,6 @@ struct ClusterJob {
   int fused_qr;           // column basis: each update pass also forms the next step's partials
   int big;                // bit 0: per-row arrays, bit 1: B[sel,:] in global memory (set by the launcher)
   cplx* Sg;               // global-slice mode: B buffer (holds B[sel,:] in big mode), stride wg_stride
-  int debug_start;        // dev aid (TTP_DEBUG_START=1|2): return start set 1 or 2
   OracleDev oracle;
   FiberJob fiber;         // index-set views and geometry (out/ld unused)
   const cplx* src;
@@ -77,11 +76,16 @@ struct ClusterJob {
   long long wg_stride;
 };
 
+#ifdef TTP_DEV
+#define TTP_DEV_CLUSTER_API int debug_phase_clocks(int enable, int64_t* out, int32_t n);
+#else
+#define TTP_DEV_CLUSTER_API
+#endif
 #define TTP_CLUSTER_API                                                                     \
   size_t cluster_smem_bytes(int m, int r, int C, bool global_slice = false, int big = 0);   \
   int pick_cluster_size(int m, int r, size_t smem_limit); /* 0 if no cluster fits */        \
   int max_active_clusters(const ClusterJob& job);                                           \
   cudaError_t launch_cluster_bond(const ClusterJob& job, int n_inst, cudaStream_t s);       \
-  int debug_phase_clocks(int enable, int64_t* out, int32_t n);
+  TTP_DEV_CLUSTER_API
 namespace ck_lat { TTP_CLUSTER_API }
 namespace ck_tp { TTP_CLUSTER_API }

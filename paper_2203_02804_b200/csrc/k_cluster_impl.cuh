@@ -49,13 +49,16 @@
 #include "ttp_internal.h"
 #include "bond_common.cuh"
 #include "fiber_fast.cuh"
+#include "dev_knobs.h"
 #include "k_bond.h"
 #include "launch.h"
 
 namespace cg = cooperative_groups;
 
+#ifdef TTP_DEV
 namespace {
-// Phase clocks of instance 0 / cluster rank 0 (diagnostic; ttp_debug_phase_clocks).
+// Phase clocks of instance 0 / cluster rank 0 (dev build only;
+// ttp_dev_phase_clocks, tools/phase_timing.py).
 __device__ long long g_phase_clock[16];
 __device__ int g_phase_enable;
 #define PHASE_MARK(k)                                                           \
@@ -78,6 +81,11 @@ __device__ unsigned long long g_sub_clock[16];
       t = _n;                                                                   \
     }                                                                           \
   } while (0)
+#else
+#define PHASE_MARK(k) do { } while (0)
+#define SP_BEGIN(t) do { } while (0)
+#define SP(t, k) do { } while (0)
+#endif
 
 namespace {
 
@@ -89,10 +97,17 @@ constexpr int RMAX = 64;
 #endif
 constexpr int QX_ROWS = QX_ROWS_DEF;  // rows per staged tile of the DMMA Q*X products
 constexpr int LAZY_MAX = 4;  // most deferred swap updates (global-slice mode)
+#ifdef TTP_DEV
 __constant__ int g_lazy_f = LAZY_MAX;  // flush cadence of the deferred updates (1 = eager)
-__constant__ int g_serpentine = 1;  // dev knob (A/B of the serpentine row order)
-__constant__ int g_swap_filter = 1;  // bound-filtered swap passes (global-slice mode); A/B knob
+__constant__ int g_serpentine = 1;  // A/B of the serpentine row order
+__constant__ int g_swap_filter = 1;  // bound-filtered swap passes (global-slice mode)
 __constant__ int g_gram_dmma = 1;   // WY Gram on DMMA (else the 4x4 scalar tiles)
+#else
+constexpr int g_lazy_f = LAZY_MAX;
+constexpr int g_serpentine = 1;
+constexpr int g_swap_filter = 1;
+constexpr int g_gram_dmma = 1;
+#endif
 
 struct __align__(16) Rec {
   double v;
@@ -2463,14 +2478,6 @@ __global__ void __launch_bounds__(CT, CLUSTER_MIN_BLOCKS) cluster_bond_kernel(Cl
     }
     __syncthreads();
     const int nstart = c.ibc[2];
-    if (J.debug_start) {  // dev aid: return a start set instead of the dominant rows
-      for (int t = threadIdx.x; t < r; t += CT) c.best[t] = c.starts[(J.debug_start - 1) * r + t];
-      __syncthreads();
-      if (job.sel_out && c.crank == 0)
-        for (int t = threadIdx.x; t < r; t += CT) job.sel_out[inst * job.sel_stride + t] = c.best[t];
-      cl.sync();
-      return;
-    }
     const long long limit = job.max_iters >= 0 ? job.max_iters : 10LL * m;
     double best_vol = -INFINITY;
     bool have = false;
@@ -2606,15 +2613,16 @@ size_t cluster_smem_bytes(int m, int r, int C, bool global_slice, int big) {
 }
 
 static size_t cluster_smem_limit() {
-  static const size_t lim = [] {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, size_t> memo;
+  return ttp_device_memo(memo, mu, 0, [] {
     int dev = 0, v = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, (const void*)cluster_bond_kernel);
     return (size_t)v - fa.sharedSizeBytes;
-  }();
-  return lim;
+  });
 }
 
 // Global-slice jobs move per-row state to global memory (the instance's
@@ -2622,7 +2630,10 @@ static size_t cluster_smem_limit() {
 // per-CTA budget of CLUSTER_MIN_BLOCKS resident CTAs per SM, or at least
 // the opt-in limit of one.
 static size_t cluster_smem_target() {
-  static const size_t t = [] {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, size_t> memo;
+  const size_t lim = cluster_smem_limit();
+  return ttp_device_memo(memo, mu, 0, [lim] {
     int dev = 0, per_sm = 0, resv = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
@@ -2630,16 +2641,15 @@ static size_t cluster_smem_target() {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, (const void*)cluster_bond_kernel);
     const long long share = (long long)per_sm / CLUSTER_MIN_BLOCKS - resv - (long long)fa.sharedSizeBytes;
-    return std::min(cluster_smem_limit(), (size_t)std::max(0LL, share));
-  }();
-  return t;
+    return std::min(lim, (size_t)std::max(0LL, share));
+  });
 }
 
 static void resolve_big(ClusterJob& job) {
   job.big = 0;
   if (!(job.Wg && job.Sg && job.b.dwork && job.b.iwork)) return;
   static const int forced = [] {  // TTP_BIG=0|1|3: A/B knob
-    const char* e = getenv("TTP_BIG");
+    const char* e = ttp_dev_env("TTP_BIG");
     return e ? atoi(e) & 3 : -1;
   }();
   if (forced >= 0 && cluster_smem_bytes(job.b.m, job.b.r, job.cl, true, forced) <= cluster_smem_limit()) {
@@ -2671,7 +2681,7 @@ int pick_cluster_size(int m, int r, size_t smem_limit) {
 // the default forms Q in compact-WY form.
 static bool q_wy_enabled() {
   static const bool on = [] {
-    const char* e = getenv("TTP_QFORM");
+    const char* e = ttp_dev_env("TTP_QFORM");
     return !(e && strcmp(e, "zung2r") == 0);
   }();
   return on;
@@ -2680,7 +2690,7 @@ static bool q_wy_enabled() {
 // TTP_STARTS=split runs the two starts as separate in-place factorizations.
 static bool fused_starts_enabled() {
   static const bool on = [] {
-    const char* e = getenv("TTP_STARTS");
+    const char* e = ttp_dev_env("TTP_STARTS");
     return !(e && strcmp(e, "split") == 0);
   }();
   return on;
@@ -2689,25 +2699,33 @@ static bool fused_starts_enabled() {
 // TTP_LAZY=F (1..LAZY_MAX): flush cadence of the deferred swap updates in
 // global-slice mode (1 = the eager update of every row pass); A/B knob.
 static cudaError_t apply_lazy_knob() {
+#ifdef TTP_DEV
   static const cudaError_t st = [] {
-    const char* e = getenv("TTP_LAZY");
+    const char* e = ttp_dev_env("TTP_LAZY");
     if (!e) return cudaSuccess;
     const int f = std::max(1, std::min(LAZY_MAX, atoi(e)));
     return cudaMemcpyToSymbol(g_lazy_f, &f, sizeof(int));
   }();
   return st;
+#else
+  return cudaSuccess;
+#endif
 }
 
 // TTP_SWAP_FILTER=0 runs every deferred swap pass over all rows (A/B knob);
 // default: bound-filtered passes between the flushing ones.
 static cudaError_t apply_swap_filter_knob() {
+#ifdef TTP_DEV
   static const cudaError_t st = [] {
-    const char* e = getenv("TTP_SWAP_FILTER");
+    const char* e = ttp_dev_env("TTP_SWAP_FILTER");
     if (!e) return cudaSuccess;
     const int f = e[0] == '0' ? 0 : 1;
     return cudaMemcpyToSymbol(g_swap_filter, &f, sizeof(int));
   }();
   return st;
+#else
+  return cudaSuccess;
+#endif
 }
 
 // TTP_FUSED_QR=0 runs the column basis with a separate partials pass per
@@ -2715,7 +2733,7 @@ static cudaError_t apply_swap_filter_knob() {
 // partials.
 static bool fused_qr_enabled() {
   static const bool on = [] {
-    const char* e = getenv("TTP_FUSED_QR");
+    const char* e = ttp_dev_env("TTP_FUSED_QR");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -2732,10 +2750,6 @@ cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream
   resolve_big(job);
   job.q_wy = q_wy_enabled() ? 1 : 0;
   job.fused_starts = fused_starts_enabled() ? 1 : 0;
-  {
-    const char* e = getenv("TTP_DEBUG_START");
-    job.debug_start = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
-  }
   const int C = job.cl;
   const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr, job.big);
   cudaError_t e = ensure_max_smem((const void*)cluster_bond_kernel);
@@ -2771,16 +2785,8 @@ int max_active_clusters(const ClusterJob& job_in) {
   const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr, job.big);
   if (smem > cluster_smem_limit()) return 0;
   static std::mutex mu;
-  static std::map<std::pair<int, size_t>, int> cache;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find({C, smem});
-    if (it != cache.end()) return it->second;
-  }
-  const int n = max_active_clusters_query(C, smem);
-  std::lock_guard<std::mutex> lk(mu);
-  cache[{C, smem}] = n;
-  return n;
+  static std::map<std::pair<int, std::pair<int, size_t>>, int> cache;
+  return ttp_device_memo(cache, mu, std::make_pair(C, smem), [&] { return max_active_clusters_query(C, smem); });
 }
 
 int max_active_clusters_query(int C, size_t smem) {
@@ -2803,6 +2809,7 @@ int max_active_clusters_query(int C, size_t smem) {
   return n;
 }
 
+#ifdef TTP_DEV
 // Phase clocks of this instantiation: out[0..16) phase marks, out[16..32)
 // sub-phase accumulators; enable also clears both.
 int debug_phase_clocks(int enable, int64_t* out, int32_t n) {
@@ -2821,5 +2828,7 @@ int debug_phase_clocks(int enable, int64_t* out, int32_t n) {
   if (cudaMemcpyToSymbol(g_phase_enable, &en, sizeof(int)) != cudaSuccess) return TTP_ERR_CUDA;
   return TTP_OK;
 }
+
+#endif
 
 }  // namespace CK_NS

@@ -8,6 +8,7 @@
 // factorizes: one thread per entry, consecutive threads on consecutive rows
 // so the complex128 stores coalesce.
 #include "ttp_internal.h"
+#include "dev_knobs.h"
 #include "launch.h"
 #include "fiber_fast.cuh"
 
@@ -122,7 +123,7 @@ __global__ void points_kernel(OracleDev o, const int* __restrict__ idx, long lon
 // TTP_FIBER_FAST=0 forces the direct per-entry evaluation (A/B checks).
 bool fiber_fast_enabled() {
   static const bool on = [] {
-    const char* e = getenv("TTP_FIBER_FAST");
+    const char* e = ttp_dev_env("TTP_FIBER_FAST");
     return !(e && e[0] == '0');
   }();
   return on;

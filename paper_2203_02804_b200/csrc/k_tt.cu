@@ -15,6 +15,7 @@
 //        s through it.  Each slice is read from HBM once per sweep instead
 //        of once per sample.
 #include "ttp_internal.h"
+#include "dev_knobs.h"
 #include "launch.h"
 #include <cooperative_groups.h>
 #include <cstring>
@@ -871,7 +872,7 @@ extern "C" int ttp_tt_inner(const ttp_tt_batch* bra, const ttp_tt_batch* ket, do
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   static const bool dmma = [] {
-    const char* e = getenv("TTP_INNER");
+    const char* e = ttp_dev_env("TTP_INNER");
     return !(e && strcmp(e, "scalar") == 0);
   }();
   if (dmma && maxb <= 32 && maxk <= 32 && tt_inner_chunk_smem() <= (size_t)lim) {

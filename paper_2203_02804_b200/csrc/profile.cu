@@ -1,6 +1,7 @@
 // Launch counting and optional per-kernel-class device timing (see launch.h).
 #include <atomic>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -66,19 +67,19 @@ LaunchScope::~LaunchScope() {
 
 cudaError_t ensure_max_smem(const void* func) {
   static std::mutex mu;
-  static std::vector<const void*> done;
-  std::lock_guard<std::mutex> lk(mu);
-  for (const void* f : done)
-    if (f == func) return cudaSuccess;
+  static std::map<std::pair<int, const void*>, bool> done;
   int dev = 0, lim = 0;
-  cudaFuncAttributes fa;
   cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, func})) return cudaSuccess;
+  cudaFuncAttributes fa;
+  e = cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, func);
   // the cap applies to dynamic shared memory on top of the static amount
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, lim - (int)fa.sharedSizeBytes);
-  if (e == cudaSuccess) done.push_back(func);
+  if (e == cudaSuccess) done[{dev, func}] = true;
   return e;
 }
 

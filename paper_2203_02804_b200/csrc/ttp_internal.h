@@ -4,6 +4,9 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/ttpricer_b200.h"
@@ -11,6 +14,21 @@
 
 int ttp_record_cuda_error(cudaError_t e);
 int ttp_fail(int status, const std::string& msg);
+
+// Host-side queries (device attributes, occupancy, function opt-ins) are
+// per-device facts: one process may drive several GPUs (torch.cuda.set_device
+// between calls), so every memo is keyed by the current device.
+template <class K, class T, class F>
+T ttp_device_memo(std::map<std::pair<int, K>, T>& memo, std::mutex& mu, const K& key, F compute) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = memo.find({dev, key});
+  if (it != memo.end()) return it->second;
+  const T v = compute();
+  memo[{dev, key}] = v;
+  return v;
+}
 
 // Raise a kernel's dynamic shared-memory cap to the device's opt-in limit,
 // once per function.  Setting it per launch to the launch's own size races

@@ -249,7 +249,7 @@ def run_cross_pair(phi_batch, v_batch, shape, cfg_phi, cfg_v, with_reports=True)
 
 
 _PER_INSTANCE = {}
-_DEVICE_TOTAL = []
+_DEVICE_TOTAL = {}
 
 
 def max_batch(shape, cfg_phi, cfg_v, n=None, fraction=0.6):
@@ -263,9 +263,10 @@ def max_batch(shape, cfg_phi, cfg_v, n=None, fraction=0.6):
     if key not in _PER_INSTANCE:
         _PER_INSTANCE[key] = cross_bytes_per_instance(shape, cfg_phi) + cross_bytes_per_instance(shape, cfg_v)
     per = _PER_INSTANCE[key]
-    if not _DEVICE_TOTAL:
-        _DEVICE_TOTAL.append(torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory)
-    if n is not None and n * per <= _DEVICE_TOTAL[0] // 3:
+    dev = torch.cuda.current_device()
+    if dev not in _DEVICE_TOTAL:
+        _DEVICE_TOTAL[dev] = torch.cuda.get_device_properties(dev).total_memory
+    if n is not None and n * per <= _DEVICE_TOTAL[dev] // 3:
         return n
     free, _ = torch.cuda.mem_get_info()
     return max(1, int(fraction * free) // max(1, per))

@@ -436,70 +436,6 @@ def test_full_size_cfg4_batch_properties():
         assert abs(P.tt_inner(tt, tt) - O.tt_inner(tt.cores, tt.cores)) <= 1e-12 * abs(O.tt_inner(tt.cores, tt.cores))
 
 
-_CK_SCRIPT = r"""
-import sys, numpy as np
-sys.path.insert(0, ".")
-import paper_2203_02804_b200 as P
-from paper_2203_02804_b200 import configs
-spec = configs.CONFIGS[4]
-shape = (spec.grid.points_per_axis,) * spec.d
-cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
-ms = [configs.make_model(4, i) for i in range(17)]
-b = P.tt_cross_batch([P.PhiGridOracle(m, spec.grid) for m in ms], shape, cfg, with_reports=False)
-assert all(s == 0 for s in b.status)
-tr = b.trains.to_trains()
-np.savez(sys.argv[1], *[c for i in (0, 8, 16) for c in tr[i].cores])
-"""
-
-
-def test_throughput_and_latency_cluster_kernels_agree(tmp_path):
-    """A cfg4 batch of 17 (global-slice clusters) gives the same cores
-    bitwise from the 256-thread two-CTAs-per-SM instantiation and the
-    512-thread one (TTP_CK forces each in its own process).  The column
-    basis runs with separate partials passes here (TTP_FUSED_QR=0): the
-    fused update pass sums its dot products per warp, so its rounding
-    depends on the CTA width."""
-    import os
-    import subprocess
-    import sys
-    script = tmp_path / "ck.py"
-    script.write_text(_CK_SCRIPT)
-    out = {}
-    for ck in ("tp", "lat"):
-        env = dict(os.environ, TTP_CK=ck, TTP_FUSED_QR="0")
-        path = tmp_path / f"{ck}.npz"
-        subprocess.run([sys.executable, str(script), str(path)], check=True, env=env,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
-        out[ck] = np.load(path)
-    assert len(out["tp"].files) == len(out["lat"].files) > 0
-    for k in out["tp"].files:
-        np.testing.assert_array_equal(out["tp"][k], out["lat"][k])
-
-
-def test_swap_filter_is_bitwise_neutral(tmp_path):
-    """The bound-filtered swap passes (global-slice mode) skip rows whose
-    bound on max|B| stays below the warp's running best; the swap sequence,
-    and so every core of a cfg4 batch of 17, is bitwise the one of the
-    unfiltered passes (TTP_SWAP_FILTER=0), on both kernel instantiations."""
-    import os
-    import subprocess
-    import sys
-    script = tmp_path / "sf.py"
-    script.write_text(_CK_SCRIPT)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for ck in ("tp", "lat"):
-        out = {}
-        for f in ("0", "1"):
-            env = dict(os.environ, TTP_CK=ck, TTP_SWAP_FILTER=f)
-            path = tmp_path / f"{ck}{f}.npz"
-            subprocess.run([sys.executable, str(script), str(path)], check=True, env=env, cwd=root,
-                           timeout=600)
-            out[f] = np.load(path)
-        assert len(out["0"].files) == len(out["1"].files) > 0
-        for k in out["0"].files:
-            np.testing.assert_array_equal(out["0"][k], out["1"][k])
-
-
 def test_throughput_kernel_batch_composition_and_properties():
     """Batches above 16 take the throughput instantiation: an instance's
     cores do not depend on its batch neighbours or position, repeated runs
@@ -525,6 +461,33 @@ def test_throughput_kernel_batch_composition_and_properties():
         idx = np.array([p + q for p in rep.left_sets[k] for q in rep.right_sets[k]])
         got, want = P.tt_evaluate_many(tt, idx), oracle(idx)
         assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))
+
+
+def test_price_independent_of_batch_size():
+    """The bond path follows the block shape only, so an option's price and
+    reports are bitwise the same whether it is priced alone, in a batch of
+    17 or in the benchmark's batch of 592 (the reference's determinism
+    contracts: test_cross.py:180-190, test_bench_cli.py:151-158)."""
+    spec = configs.CONFIGS[4]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    models = [configs.make_model(4, i) for i in range(592)]
+    alone = P.price_fourier_tt(models[0], spec.grid, cfg, cfg, dense_reference="never")
+    alone16 = P.price_fourier_tt(models[16], spec.grid, cfg, cfg, dense_reference="never")
+    b17 = P.price_fourier_tt_batch(models[:17], spec.grid, cfg, cfg)
+    b592 = P.price_fourier_tt_batch(models, spec.grid, cfg, cfg)
+    for one, i in ((alone, 0), (alone16, 16)):
+        assert one.price == b17[i].price == b592[i].price
+        assert one.diagnostics["imag_part"] == b17[i].diagnostics["imag_part"] == b592[i].diagnostics["imag_part"]
+        for key in ("cross_phi", "cross_v"):
+            assert one.diagnostics[key].to_dict() == b592[i].diagnostics[key].to_dict()
+            assert one.diagnostics[key].left_sets == b592[i].diagnostics[key].left_sets
+    # small blocks (cfg2, the one-CTA kernel): alone == inside a batch
+    spec = configs.CONFIGS[2]
+    cfg = P.CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed)
+    models = [configs.make_model(3, i) for i in range(40)]
+    batch = P.price_fourier_tt_batch(models, spec.grid, cfg, cfg)
+    for i in (0, 39):
+        assert P.price_fourier_tt(models[i], spec.grid, cfg, cfg, dense_reference="never").price == batch[i].price
 
 
 def test_batch_prices_equal_single_prices():
