@@ -169,6 +169,28 @@ int ttp_profile_read(ttp_kernel_stat* out, int32_t max_entries);
 int ttp_oracle_eval(const ttp_oracle* oracle, const int32_t* d_shape, int32_t n_inst,
                     const int32_t* d_idx, int64_t m, double* d_out, void* stream);
 
+/* K1/K2 at one sampled unfolding block per instance -- the reference's
+ * _block (cross.py:310-332) plus its single oracle call, evaluated by the
+ * SAME separable device code the bond kernels use to fill their blocks
+ * (fiber_fast.cuh: the v0 path's fiber kernel and the cluster kernels'
+ * load_block share phi_part / vhat_part / *_combine, op for op).
+ * The sampled axis sits at position `axis` of the multi-index: left tuples
+ * have `axis` entries (d_left: n_left x axis int32, row-major), right tuples
+ * d - axis - 1 (d_right: n_right x (d - axis - 1)); both are shared by all
+ * instances.  Entry (a, s, b) = oracle_i(left[a] ++ (s) ++ right[b]).
+ *   layout 0 (left-to-right sweep, cross.py:412-423): the tall matrix has
+ *            rows a*n + s and columns b   ((n_left*n) x n_right);
+ *   layout 1 (right-to-left sweep, cross.py:424-435): rows s*n_right + b
+ *            and columns a                ((n*n_right) x n_left), i.e. the
+ *            transpose of _block(..., axis_first=True) that _interp_core
+ *            receives (cross.py:428).
+ * d_out[i*out_stride + col*rows + row]: each instance's tall matrix,
+ * column-major (the bond kernels' layout).                                */
+int ttp_eval_fibers(const ttp_oracle* oracle, const int32_t* d_shape, int32_t n_inst, int32_t layout,
+                    int32_t axis, int32_t axis_size, const int32_t* d_left, int32_t n_left,
+                    const int32_t* d_right, int32_t n_right, double* d_out, int64_t out_stride,
+                    void* stream);
+
 /* K7: batched tt_inner(bra, ket) = sum conj(bra[idx]) ket[idx]
  * (tensor_train.py:143-159); d_out holds n_inst complex values.            */
 int ttp_tt_inner(const ttp_tt_batch* bra, const ttp_tt_batch* ket, double* d_out,

@@ -159,6 +159,8 @@ SIGNATURES = [
     ("ttp_profile_reset", None, []),
     ("ttp_profile_read", _i32, [ctypes.POINTER(KernelStat), _i32]),
     ("ttp_oracle_eval", _i32, [ctypes.POINTER(Oracle), _p, _i32, _p, _i64, _p, _p]),
+    ("ttp_eval_fibers", _i32, [ctypes.POINTER(Oracle), _p, _i32, _i32, _i32, _i32, _p, _i32, _p, _i32,
+                                _p, _i64, _p]),
     ("ttp_tt_inner", _i32, [ctypes.POINTER(TTBatch), ctypes.POINTER(TTBatch), _p, _p]),
     ("ttp_tt_eval_workspace", _sz, [ctypes.POINTER(TTBatch), _i64]),
     ("ttp_tt_eval", _i32, [ctypes.POINTER(TTBatch), _p, _i64, _p, _p, _sz, _p]),

@@ -23,7 +23,8 @@ from .errors import MaxvolIterationError, OracleBudgetError, SingularMatrixError
 from .oracles import OracleBatch, check_device_oracle
 from .tensor_train import DeviceTTBatch, TensorTrain, sample_indices
 
-__all__ = ["CrossConfig", "CrossReport", "maxvol", "tt_cross", "tt_cross_batch", "CrossBatchResult"]
+__all__ = ["CrossConfig", "CrossReport", "maxvol", "tt_cross", "tt_cross_batch", "CrossBatchResult",
+           "sample_block"]
 
 COND_LIMIT = 1e12
 RANK_TOL = 1e-12
@@ -117,6 +118,27 @@ class CrossReport:
             "final_diff": self.final_diff,
             "compression_ratio": self.compression_ratio,
         }
+
+
+def sample_block(oracle, left, axis_size, right, axis_first):
+    """One bond's sampled unfolding on the GPU -- the reference's ``_block``
+    (cross.py:310-332): rows ``left x axis`` and columns ``right`` when
+    ``axis_first`` is False (left-to-right sweep), rows ``left`` and columns
+    ``axis x right`` when True.  Returns ``(block, row_tuples, col_tuples)``
+    in the reference's orientation.  The values come from ttp_eval_fibers,
+    i.e. the separable evaluation the bond kernels fill their blocks with."""
+    o = check_device_oracle(oracle)
+    left = [tuple(int(v) for v in t) for t in left]
+    right = [tuple(int(v) for v in t) for t in right]
+    axis = len(left[0])
+    if len(right[0]) != o.d - axis - 1 or any(len(t) != axis for t in left):
+        raise ValueError("left/right tuples do not span the oracle's dimension")
+    shape = list(o.shape) if o.shape is not None else [int(axis_size)] * o.d
+    shape[axis] = int(axis_size)
+    tall = OracleBatch([o]).fiber_blocks(left, right, axis, shape, 1 if axis_first else 0)[0]
+    if axis_first:
+        return tall.T, left, [(s,) + b for s in range(axis_size) for b in right]
+    return tall, [a + (s,) for a in left for s in range(axis_size)], right
 
 
 def rank_profile(shape, bond_dim):

@@ -145,6 +145,38 @@ extern "C" int ttp_oracle_eval(const ttp_oracle* oracle, const int32_t* d_shape,
   return TTP_OK;
 }
 
+extern "C" int ttp_eval_fibers(const ttp_oracle* oracle, const int32_t* d_shape, int32_t n_inst,
+                               int32_t layout, int32_t axis, int32_t axis_size, const int32_t* d_left,
+                               int32_t n_left, const int32_t* d_right, int32_t n_right, double* d_out,
+                               int64_t out_stride, void* stream) {
+  if (!oracle || oracle->d < 1 || oracle->d > TTP_MAX_D || n_inst < 0 || n_left < 1 || n_right < 1 ||
+      axis_size < 1 || axis < 0 || axis >= oracle->d || (layout != 0 && layout != 1) || !d_out)
+    return ttp_fail(TTP_ERR_INVALID, "eval_fibers: invalid arguments");
+  if (oracle->kind < TTP_ORACLE_PHI_GBM || oracle->kind > TTP_ORACLE_TABLE)
+    return ttp_fail(TTP_ERR_INVALID, "eval_fibers: unknown oracle kind");
+  const long long rows = layout == 0 ? (long long)n_left * axis_size : (long long)axis_size * n_right;
+  const long long cols = layout == 0 ? n_right : n_left;
+  if (out_stride < rows * cols) return ttp_fail(TTP_ERR_INVALID, "eval_fibers: out_stride too small");
+  if (n_inst == 0) return TTP_OK;
+  OracleDev o = oracle_dev_from(*oracle, d_shape);
+  FiberJob f{};
+  f.mode = layout;
+  f.rl = n_left;
+  f.na = axis_size;
+  f.rr = n_right;
+  f.kl = axis;
+  // the index sets are shared by all instances (set_stride 0), rows packed
+  // at their tuple length
+  f.left = SetView{d_left, 0, 0, axis};
+  f.right = SetView{d_right, 0, 0, oracle->d - axis - 1};
+  f.out = reinterpret_cast<cplx*>(d_out);
+  f.out_stride = out_stride;
+  f.ld = rows;
+  launch_fiber(o, f, nullptr, n_inst, (cudaStream_t)stream);
+  TTP_CUDA_CHECK(cudaGetLastError());
+  return TTP_OK;
+}
+
 extern "C" int ttp_cross_layout_of(int32_t d, const int32_t* h_shape, int32_t bond_dim,
                                    ttp_cross_layout* out) {
   if (d < 1 || d > TTP_MAX_D || bond_dim < 1 || bond_dim > 64 || !h_shape || !out)

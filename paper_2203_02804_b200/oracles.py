@@ -210,6 +210,44 @@ class OracleBatch:
 
     def evaluate(self, idx, shape):
         """Values of every instance at the shared indices -> (n_inst, m) numpy."""
+        m = np.asarray(idx).shape[0]
+        return self.evaluate_device(idx, shape)[:, :m].cpu().numpy()
+
+    def fiber_blocks(self, left, right, axis, shape, layout):
+        """Sampled unfolding block of every instance (ttp_eval_fibers, the
+        bond kernels' own separable evaluation; reference _block,
+        cross.py:310-332).  ``left``: (n_left, axis) and ``right``:
+        (n_right, d - axis - 1) integer tuples shared by all instances.
+        Returns (n_inst, rows, cols) complex numpy: layout 0 rows a*n + s,
+        columns b; layout 1 rows s*n_right + b, columns a (the transpose of
+        the reference's axis-first block, as _interp_core receives it)."""
+        torch = _lib.require_device()
+        lib = _lib.load_library()
+        shape = tuple(int(n) for n in shape)
+        n = shape[axis]
+        left = np.asarray(left, dtype=np.int64).reshape(-1, axis)
+        right = np.asarray(right, dtype=np.int64).reshape(-1, self.d - axis - 1)
+        for tup, lo in ((left, 0), (right, axis + 1)):
+            for j in range(tup.shape[1]):
+                if tup.size and (tup[:, j].min() < 0 or tup[:, j].max() >= shape[lo + j]):
+                    raise IndexError(f"axis {lo + j}: index out of range [0, {shape[lo + j]})")
+        nl, nr = left.shape[0], right.shape[0]
+        rows, cols = (nl * n, nr) if layout == 0 else (n * nr, nl)
+        dev = torch.device("cuda")
+        d_left = torch.from_numpy(np.ascontiguousarray(left.astype(np.int32)).reshape(-1)).to(dev)
+        d_right = torch.from_numpy(np.ascontiguousarray(right.astype(np.int32)).reshape(-1)).to(dev)
+        d_shape = torch.tensor(shape, dtype=torch.int32, device=dev)
+        out = torch.empty((self.n_inst, cols, rows), dtype=torch.complex128, device=dev)
+        st = lib.ttp_eval_fibers(ctypes.byref(self.struct), ctypes.c_void_p(d_shape.data_ptr()),
+                                 self.n_inst, int(layout), int(axis), n,
+                                 ctypes.c_void_p(d_left.data_ptr() if d_left.numel() else d_shape.data_ptr()),
+                                 nl, ctypes.c_void_p(d_right.data_ptr() if d_right.numel() else d_shape.data_ptr()),
+                                 nr, ctypes.c_void_p(out.data_ptr()), rows * cols, _lib.stream_handle())
+        _lib.raise_for(st, "fiber evaluation")
+        return out.transpose(1, 2).cpu().numpy()  # column-major -> (rows, cols)
+
+    def evaluate_device(self, idx, shape):
+        """Values at the shared indices as a (n_inst, max(m, 1)) device tensor."""
         torch = _lib.require_device()
         lib = _lib.load_library()
         idx = np.asarray(idx, dtype=np.int64)
@@ -228,4 +266,4 @@ class OracleBatch:
                                  self.n_inst, ctypes.c_void_p(d_idx.data_ptr()), m,
                                  ctypes.c_void_p(out.data_ptr()), _lib.stream_handle())
         _lib.raise_for(st, "oracle evaluation")
-        return out[:, :m].cpu().numpy()
+        return out

@@ -239,8 +239,7 @@ def tt_rand_sample_diff(tt, oracle, m, seed):
     _check_bonds(tt)
     batch = DeviceTTBatch.from_trains([tt])
     approx = _device_eval(batch, idx)
-    exact_np = OracleBatch([oracle]).evaluate(idx, tt.phys_dims)
-    exact = torch.from_numpy(exact_np).to("cuda")
+    exact = OracleBatch([oracle]).evaluate_device(idx, tt.phys_dims)[0, :m].contiguous()
     ws = torch.empty(16, dtype=torch.float64, device="cuda")
     out = (ctypes.c_double * 1)()
     st = lib.ttp_sample_diff(1, m, ctypes.c_void_p(exact.data_ptr()),
