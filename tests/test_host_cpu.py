@@ -174,6 +174,23 @@ def test_json_container_roundtrip(tmp_path):
         np.testing.assert_array_equal(a, b)
 
 
+def test_json_interchange_with_reference(tmp_path):
+    """a container written by the REFERENCE's tt_save_json
+    (tests/golden/ref_tt.json, tensor_train.py:228-245) loads into the same
+    cores here, and this package's writer produces byte-identical files (the
+    generator, make_golden_r02.py json, also reads the repo's output back
+    with the reference's tt_load_json)."""
+    import os
+    from conftest import GOLDEN
+    want = np.load(os.path.join(GOLDEN, "ref_tt_cores.npy"))
+    back = tt_load_json(os.path.join(GOLDEN, "ref_tt.json"))
+    np.testing.assert_array_equal(np.concatenate([c.ravel() for c in back.cores]), want)
+    assert back.phys_dims == (5, 2, 6, 3) and back.bond_dims == (1, 3, 4, 2, 1)
+    path = tmp_path / "repo.json"
+    tt_save_json(back, path)
+    assert path.read_text() == open(os.path.join(GOLDEN, "ref_tt.json")).read()
+
+
 def test_tensor_train_container_rules():
     with pytest.raises(ValueError, match="bond mismatch"):
         TensorTrain([np.zeros((1, 2, 3)), np.zeros((4, 2, 1))])

@@ -126,3 +126,22 @@ def test_cfg4_noise_band_fixture_is_pinned(golden):
     assert band["unperturbed"] == golden["prices"]["cfg4_i0"]["price"]
     assert len(band["rel_dev_sorted"]) >= 10
     assert max(band["rel_dev_sorted"]) <= 4e-5
+
+
+def test_oracle_reproduces_round2_reference_prices():
+    """The per-instance P4 bands (noise_bands.json) were measured around the
+    oracle's unperturbed price; the reference's own price_fourier_tt
+    (ref_prices_r02.json) must be that same number, bit for bit.  Checked
+    here on the fast configs (the generator checked all 28)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    ref = json.load(open(os.path.join(GOLDEN, "ref_prices_r02.json")))
+    bands = json.load(open(os.path.join(GOLDEN, "noise_bands.json")))
+    for key in ref:
+        if key.startswith("cfg"):
+            assert bands[key]["unperturbed"] == ref[key]["price"]
+    for cid, inst in ((2, 1), (3, 0)):
+        spec = configs.CONFIGS[cid]
+        price, _ = O.price_tt(grid_model(cid, inst), spec.bond_dim, spec.bond_dim, spec.cross_seed, spec.cross_seed)
+        assert price == ref[f"cfg{cid}_i{inst}"]["price"]
