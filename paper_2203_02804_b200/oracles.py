@@ -225,8 +225,10 @@ class OracleBatch:
         lib = _lib.load_library()
         shape = tuple(int(n) for n in shape)
         n = shape[axis]
-        left = np.asarray(left, dtype=np.int64).reshape(-1, axis)
-        right = np.asarray(right, dtype=np.int64).reshape(-1, self.d - axis - 1)
+        left = np.asarray(left, dtype=np.int64)
+        right = np.asarray(right, dtype=np.int64)
+        left = left.reshape(left.shape[0] if left.ndim else 1, axis)
+        right = right.reshape(right.shape[0] if right.ndim else 1, self.d - axis - 1)
         for tup, lo in ((left, 0), (right, axis + 1)):
             for j in range(tup.shape[1]):
                 if tup.size and (tup[:, j].min() < 0 or tup[:, j].max() >= shape[lo + j]):

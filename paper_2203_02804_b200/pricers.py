@@ -201,14 +201,15 @@ def price_fourier_dense(model, grid, t=0.0, term_cap=DENSE_TERM_CAP):
 _PAIR_STREAMS = {}
 
 
-def run_cross_pair(phi_batch, v_batch, shape, cfg_phi, cfg_v, with_reports=True):
+def run_cross_pair(phi_batch, v_batch, shape, cfg_phi, cfg_v, with_reports=True, concurrent=True):
     """The two independent crosses of price_fourier_tt (pricers.py:271-272)
     issued from two host threads on two CUDA streams, so the phi and vhat
     sweeps overlap on the GPU (each sweep driver blocks its own thread on the
-    per-sweep convergence read-back).  Returns (phi_result, v_result)."""
+    per-sweep convergence read-back).  Returns (phi_result, v_result).
+    ``concurrent=False`` runs them one after the other on the caller's
+    stream (bench.py's per-kernel timing step); results are identical."""
     torch = _lib.require_device()
-    import os
-    if os.environ.get("TTP_PAIR_STREAMS", "1") == "0":  # diagnostics: serialize the two crosses
+    if not concurrent:
         return (tt_cross_batch(phi_batch, shape, cfg_phi, with_reports=with_reports),
                 tt_cross_batch(v_batch, shape, cfg_v, with_reports=with_reports))
     dev = torch.cuda.current_device()
@@ -273,14 +274,27 @@ def max_batch(shape, cfg_phi, cfg_v, n=None, fraction=0.6):
 
 
 def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference="never",
-                           term_cap=DENSE_TERM_CAP, raise_errors=True):
+                           term_cap=DENSE_TERM_CAP, raise_errors=True, group=None):
     """Price many independent options on one grid with the device TT path.
 
     All instances share the grid and the two CrossConfigs (so they share the
     seeded pivot initialisation and convergence samples); parameters differ
     per instance.  Returns a list of PricingResult (or exceptions when
     ``raise_errors`` is False).
+
+    ``group``: a torch.distributed process group (e.g. ``dist.group.WORLD``,
+    one rank per GPU).  Every rank then passes the same full batch, prices
+    its contiguous share on its own GPU, and one all-gather of a small
+    per-option record returns the whole batch, in order, on every rank
+    (distributed.price_batch_sharded).  Because the kernel
+    path depends only on block shapes, each price is bitwise the one a
+    single GPU computes.
     """
+    if group is not None:
+        if dense_reference != "never":
+            raise ValueError("the sharded batch pricer takes dense_reference='never'")
+        from .distributed import price_batch_sharded
+        return price_batch_sharded(models, grid, cfg_phi, cfg_v, t=t, group=group, raise_errors=raise_errors)
     for m in models:
         if m.d != grid.d:
             raise ValueError(f"model has d={m.d} but grid has d={grid.d}")

@@ -44,21 +44,23 @@ def run(job):
             return g_
         gm.phi_oracle = lambda: noisy(phi0)
         gm.vhat_oracle = lambda: noisy(v0)
-    price, _ = O.price_tt(gm, spec.bond_dim, spec.bond_dim, spec.cross_seed, spec.cross_seed)
-    return job, price
+    price, info = O.price_tt(gm, spec.bond_dim, spec.bond_dim, spec.cross_seed, spec.cross_seed)
+    return job, (price, {k: {"sweeps_used": int(info[k]["sweeps_used"]), "final_diff": float(info[k]["final_diff"])}
+                         for k in ("cross_phi", "cross_v")})
 
 
 if __name__ == "__main__":
     cid, n_inst, n_seeds = (int(a) for a in sys.argv[1:4])
     jobs = [(cid, i, s) for i in range(n_inst) for s in [-1] + list(range(n_seeds))]
-    with ProcessPoolExecutor(max_workers=os.cpu_count()) as ex:
+    with ProcessPoolExecutor(max_workers=int(os.environ.get('BAND_WORKERS', os.cpu_count()))) as ex:
         res = dict(ex.map(run, jobs))
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
     for i in range(n_inst):
-        base = res[(cid, i, -1)]
-        rel = sorted(abs(res[(cid, i, s)] - base) / abs(base) for s in range(n_seeds))
+        base = res[(cid, i, -1)][0]
+        rel = sorted(abs(res[(cid, i, s)][0] - base) / abs(base) for s in range(n_seeds))
         data[f"cfg{cid}_i{i}"] = {"unperturbed": base, "rel_dev_sorted": rel, "max": max(rel),
-                                  "median": float(np.median(rel)), "n_seeds": n_seeds}
+                                  "median": float(np.median(rel)), "n_seeds": n_seeds,
+                                  "reports": [res[(cid, i, s)][1] for s in [-1] + list(range(n_seeds))]}
         print(f"cfg{cid} i{i}: price {base!r} noise max {max(rel):.2e} median {np.median(rel):.2e}")
     data["generator"] = ("tests/golden/make_noise_band.py CID N_INST N_SEEDS (OPENBLAS_NUM_THREADS=1): "
                          "the pinned restatement with 1e-15 relative oracle noise")

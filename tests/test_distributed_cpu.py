@@ -151,3 +151,141 @@ def test_gloo_world2_split_crosses():
     gm = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, spec.grid.n, spec.grid.eta, spec.grid.alpha)
     want, _ = O.price_tt(gm, spec.bond_dim, spec.bond_dim, spec.cross_seed, spec.cross_seed, n_conv=2000)
     assert p0 == pytest.approx(want, rel=1e-13)
+
+
+def _cpu_pricer(models, grid, cfg_phi, cfg_v, t=0.0, raise_errors=True):
+    """CPU stand-in for the device batch pricer (same signature and result
+    shape as price_fourier_tt_batch): the pinned restatement per option; a
+    strike of 77 raises OracleBudgetError to exercise the error path."""
+    from oracle import ttp_oracle as O
+    from paper_2203_02804_b200 import CrossReport, OracleBudgetError, PricingResult
+    out = []
+    for m in models:
+        if m.strike == 77.0:
+            out.append(OracleBudgetError("injected budget failure"))
+            continue
+        gm = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, grid.n, grid.eta, grid.alpha)
+        price, info = O.price_tt(gm, cfg_phi.bond_dim, cfg_v.bond_dim, cfg_phi.seed, cfg_v.seed, t=t,
+                                 n_conv=cfg_phi.n_conv_samples)
+
+        def rep(r, cfg):
+            return CrossReport(converged=bool(r["converged"]), sweeps_used=int(r["sweeps_used"]),
+                               oracle_calls=int(r["oracle_calls"]), conv_check_calls=int(r["conv_check_calls"]),
+                               final_diff=float(r["final_diff"]),
+                               compression_ratio=int(r["oracle_calls"]) / grid.n_terms)
+        value = gm.prefactor(t) * info["raw"]
+        out.append(PricingResult(price, "fourier_tt", 0.0, {
+            "cross_phi": rep(info["cross_phi"], cfg_phi), "cross_v": rep(info["cross_v"], cfg_v),
+            "imag_part": float(value.imag), "oracle_calls_total": 0}))
+    if raise_errors:
+        for r in out:
+            if isinstance(r, Exception):
+                raise r
+    return out
+
+
+def _models_cfg1(n, bad=None):
+    from paper_2203_02804_b200 import MarketModel, configs
+    out = []
+    for i in range(n):
+        m = configs.make_model(3, i)
+        if i == bad:
+            m = MarketModel(r=m.r, sigma=m.sigma, T=m.T, s0=m.s0, strike=77.0, corr=m.corr, d=m.d)
+        out.append(m)
+    return out
+
+
+def _sharded_worker(rank, world, port, out_path, n, bad):
+    import pickle
+    import torch.distributed as dist
+    from paper_2203_02804_b200 import CrossConfig, GridSpec
+    from paper_2203_02804_b200.distributed import price_batch_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    grid = GridSpec(n=8, eta=0.3, alpha=1.0, d=5)
+    cfg = CrossConfig(bond_dim=4, seed=1239, n_conv_samples=500)
+    models = _models_cfg1(n, bad)
+    res = {"rank": rank}
+    try:
+        out = price_batch_sharded(models, grid, cfg, cfg, group=dist.group.WORLD, local_pricer=_cpu_pricer)
+        res["prices"] = [r.price for r in out]
+        res["owners"] = [r.diagnostics.get("rank", rank) for r in out]
+        res["reports"] = [r.diagnostics["cross_phi"].to_dict() for r in out]
+    except Exception as exc:  # noqa: BLE001 - recorded for the assertion
+        res["error"] = type(exc).__name__
+    with open(out_path + f".{rank}.pkl", "wb") as fh:
+        pickle.dump(res, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [5, 6])
+def test_gloo_world2_sharded_batch_api(tmp_path, n):
+    """price_fourier_tt_batch(..., group=...) -> distributed.price_batch_sharded:
+    both ranks get the whole batch in input order, identical prices, each
+    option priced by its contiguous owner; the gathered records rebuild the
+    reports' counters exactly."""
+    import pickle
+    from paper_2203_02804_b200 import CrossConfig, GridSpec
+    out = str(tmp_path / "sh")
+    mp.spawn(_sharded_worker, args=(2, _free_port(), out, n, None), nprocs=2, join=True)
+    r0, r1 = (pickle.load(open(out + f".{r}.pkl", "rb")) for r in (0, 1))
+    assert "error" not in r0 and "error" not in r1
+    assert r0["prices"] == r1["prices"] and r0["reports"] == r1["reports"]
+    assert r0["owners"] == r1["owners"] == [0] * (n // 2) + [1] * (n - n // 2)
+    grid = GridSpec(n=8, eta=0.3, alpha=1.0, d=5)
+    cfg = CrossConfig(bond_dim=4, seed=1239, n_conv_samples=500)
+    want = _cpu_pricer(_models_cfg1(n), grid, cfg, cfg)
+    assert r0["prices"] == [w.price for w in want]
+    assert r0["reports"] == [w.diagnostics["cross_phi"].to_dict() for w in want]
+
+
+def test_gloo_world2_sharded_batch_error_raises_on_every_rank(tmp_path):
+    """An option failing on rank 1 is raised on BOTH ranks (same class) after
+    the one collective -- no rank is left blocked in the all-gather."""
+    import pickle
+    out = str(tmp_path / "err")
+    mp.spawn(_sharded_worker, args=(2, _free_port(), out, 6, 4), nprocs=2, join=True)
+    r0, r1 = (pickle.load(open(out + f".{r}.pkl", "rb")) for r in (0, 1))
+    assert r0["error"] == r1["error"] == "OracleBudgetError"
+
+
+def _split2_err_worker(rank, world, port, out_path):
+    import pickle
+    import torch.distributed as dist
+    from paper_2203_02804_b200 import CrossConfig, SingularMatrixError, configs
+    from paper_2203_02804_b200.distributed import price_fourier_tt_split2
+    from paper_2203_02804_b200.oracles import PhiGridOracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def cross_fn(o, shape, cfg):
+        if not isinstance(o, PhiGridOracle):
+            raise SingularMatrixError("injected", bond=2)
+        from paper_2203_02804_b200 import TensorTrain
+        return TensorTrain([np.ones((1, n, 1), complex) for n in shape])
+
+    spec = configs.CONFIGS[1]
+    cfg = CrossConfig(bond_dim=spec.bond_dim, seed=spec.cross_seed, n_conv_samples=2000)
+    res = {}
+    try:
+        price_fourier_tt_split2(configs.make_model(1), spec.grid, cfg, cfg, cross_fn=cross_fn,
+                                inner_fn=lambda a, b: 1.0)
+    except Exception as exc:  # noqa: BLE001
+        res["error"] = type(exc).__name__
+    with open(out_path + f".{rank}.pkl", "wb") as fh:
+        pickle.dump(res, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_split_crosses_error_does_not_hang(tmp_path):
+    """If the vhat cross raises on rank 1, rank 0 raises too instead of
+    waiting forever for the cores (status word exchanged first)."""
+    import pickle
+    out = str(tmp_path / "s2e")
+    mp.spawn(_split2_err_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r0, r1 = (pickle.load(open(out + f".{r}.pkl", "rb")) for r in (0, 1))
+    assert r0["error"] == r1["error"] == "SingularMatrixError"

@@ -21,7 +21,7 @@ from paper_2203_02804_b200 import configs
 
 pytestmark = pytest.mark.gpu
 
-BAND_FACTOR = 3.0
+BAND_FACTOR = 2.0
 
 
 def _golden():
