@@ -1,29 +1,37 @@
 #!/usr/bin/env python
-"""Benchmark: options priced per second at d=10, N=128, TT rank <= 32.
+"""Benchmark: options priced per second through the TT-Fourier hot path.
 
 BASELINE.json's metric is quoted on config 4 (d=10 call-on-min, 129 points
-per axis, bond dimension 32).  One *step* prices one batch of ``--batch``
-independent config-4-type options per GPU (instance i has parameters drawn
-from ``default_rng([4, i])``) through the full hot path:
+per axis, bond dimension 32), the default here; ``--config {1,2,3,5}``
+measures the other BASELINE configurations with the same JSON contract.  One
+*step* prices one batch of independent options through the full hot path:
 TT-cross of phi(-z), TT-cross of conj(vhat(z)), tt_inner, prefactor.
+Instance i of config c draws its parameters from ``default_rng([c, i])``
+(SURVEY.md 8(d)).
 
   value   device throughput with the option parameters already resident in
           HBM (CUDA events, barrier + synchronize around exactly K steps,
-          max over ranks); weak scaling across GPUs.
-  e2e     the same metric through the public API with host inputs
-          (``price_fourier_tt_batch``): parameter upload and price/report
-          download inside the timed region.
+          max over ranks).  Configs 1, 2, 4, 5: a fixed batch per GPU (weak
+          scaling).  Config 3: BASELINE's 4096-instance batch split over the
+          GPUs (strong scaling).
+  e2e     the same metric through the public API with host inputs:
+          ``price_fourier_tt_batch(models, ..., group=WORLD)`` on every rank
+          (each prices its contiguous share, one all-gather of the records).
+  parity  the timed batch's first prices against the REFERENCE's own prices
+          of the same instances (tests/golden/ref_prices_r02.json, made by
+          ttpricer.price_fourier_tt) or, where no golden exists, the live CPU
+          port; each within twice that instance's reference noise band
+          (tests/golden/noise_bands.json).  Exit status 3 when outside.
   --impl reference
-          the reference algorithm on the host CPU cores (the pinned oracle
-          port, oracle/ttp_oracle.py -- the reference is pure Python and does
-          not travel to the GPU box), one option per core per step.
+          the reference algorithm on the host CPU cores: its pinned numpy
+          restatement (oracle/ttp_oracle.py -- the reference is pure Python and
+          does not travel to the GPU box), one option per core.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -34,10 +42,19 @@ import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
-
-CONFIG_ID = 4
-METRIC = "options priced/sec at d=10, N=128, TT rank<=32"
 UNIT = "options/s"
+
+# per BASELINE config: metric, default per-GPU batch (global for strong
+# scaling), scaling, CPU-sample size (None = one option per host core)
+META = {
+    1: dict(metric="options priced/sec at d=3, N=32, TT rank<=10", batch=1024, scaling="weak", cpu=lambda c: 8 * c),
+    2: dict(metric="options priced/sec at d=5, N=64, TT rank<=20", batch=1024, scaling="weak", cpu=lambda c: c),
+    3: dict(metric="options priced/sec, 4096-instance d=5 batch, N=64, TT rank<=20", batch=4096,
+            scaling="strong", cpu=lambda c: 64),
+    4: dict(metric="options priced/sec at d=10, N=128, TT rank<=32", batch=592, scaling="weak", cpu=lambda c: c),
+    5: dict(metric="options priced/sec at d=20, N=256, TT rank<=64", batch=148, scaling="weak", cpu=lambda c: c),
+}
+BAND_FACTOR = 2.0  # parity: within twice the instance's reference noise band
 
 
 # ------------------------------------------------------------------ helpers
@@ -47,24 +64,36 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--batch", type=int, default=592,
-                    help="options per GPU per step (4 x 148: throughput saturates here, profiles/r01/batch_sweep.json)")
+    ap.add_argument("--config", type=int, default=4, choices=sorted(META))
+    ap.add_argument("--batch", type=int, default=0,
+                    help="options per GPU per step (config 3: global); 0 = the config's default "
+                         "(cfg4: 4 x 148, where throughput saturates, profiles/r01/batch_sweep.json)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=0, help="options in the CPU baseline sample (0 = one per core)")
-    return ap.parse_args()
+    ap.add_argument("--cpu-sample", type=int, default=0, help="options in the CPU sample (0 = config default)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        print("note: timing rules ask for >= 3 warm-up steps", file=sys.stderr)
+    return args
 
 
 def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def spec():
+def spec_of(cid):
     from paper_2203_02804_b200 import configs
-    return configs.CONFIGS[CONFIG_ID]
+    return configs.CONFIGS[cid]
+
+
+def batches(args, world):
+    """(per-GPU batch on this rank's range, global batch)."""
+    meta = META[args.config]
+    b = args.batch or meta["batch"]
+    if meta["scaling"] == "strong":
+        return None, b
+    return b, b * world
 
 
 class ClockSampler:
@@ -112,20 +141,57 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def alg_work_per_instance(sp, sweeps_phi, sweeps_v):
-    """Algorithmic FP64 flops per option (SURVEY.md 8(d) formulas)."""
+# ------------------------------------------------------ algorithmic work
+def block_shapes(sp, direction):
+    """(m, r) of every bond block of one directional sweep (cross.py:412-435)."""
     from paper_2203_02804_b200.cross import rank_profile
     d, n = sp.d, sp.grid.points_per_axis
     r = rank_profile((n,) * d, sp.bond_dim)
-    m_conv = 50_000
-    la = 0.0
-    for k in range(1, d):
-        la += 44.0 * (r[k - 1] * n) * r[k] ** 2           # left-to-right bonds
-    conv = 8.0 * m_conv * sum(r[k] * r[k + 1] for k in range(1, d))
-    inner = 8.0 * sum(n * (r[k] * r[k] * r[k + 1] + r[k] * r[k + 1] * r[k + 1]) for k in range(d))
-    per_sweep = la + conv
-    return {"bond_la": la, "conv": conv, "inner": inner,
-            "total": per_sweep * (sweeps_phi + sweeps_v) + inner}
+    if direction == 0:
+        return [(r[k - 1] * n, r[k]) for k in range(1, d)]
+    return [(n * r[k + 1], r[k]) for k in range(d - 1, 0, -1)]
+
+
+def sweep_work(sp, direction):
+    """Algorithmic work of one directional sweep of one cross:
+    bond linear algebra 44 m r^2 flops per bond, split by the kernel that runs
+    it (blocks >= 1 MB: cluster kernel, else the one-CTA kernel, as
+    driver.cu:run_bond decides), fiber bytes (16 per sampled entry, the last
+    core included), convergence check 8 M sum r_k r_k+1 flops."""
+    from paper_2203_02804_b200.cross import rank_profile
+    d, n = sp.d, sp.grid.points_per_axis
+    r = rank_profile((n,) * d, sp.bond_dim)
+    cluster = v0 = 0.0
+    entries = 0
+    for m, rk in block_shapes(sp, direction):
+        f = 44.0 * m * rk * rk
+        if m * rk * 16 >= (1 << 20):
+            cluster += f
+        else:
+            v0 += f
+        entries += m * rk
+    entries += (r[d - 1] * n) if direction == 0 else (n * r[1])
+    conv = 8.0 * 50_000 * sum(r[k] * r[k + 1] for k in range(1, d))
+    return {"cluster": cluster, "v0": v0, "fiber_bytes": 16.0 * entries, "conv": conv}
+
+
+def inner_flops(sp):
+    from paper_2203_02804_b200.cross import rank_profile
+    d, n = sp.d, sp.grid.points_per_axis
+    r = rank_profile((n,) * d, sp.bond_dim)
+    return 8.0 * sum(n * (r[k] * r[k] * r[k + 1] + r[k] * r[k + 1] * r[k + 1]) for k in range(d))
+
+
+def work_of_batch(sp, sweeps_phi, sweeps_v):
+    """Summed algorithmic work of a batch given each instance's sweep counts."""
+    per_dir = [sweep_work(sp, 0), sweep_work(sp, 1)]
+    tot = {"cluster": 0.0, "v0": 0.0, "fiber_bytes": 0.0, "conv": 0.0}
+    for s in list(sweeps_phi) + list(sweeps_v):
+        for q in range(int(s)):
+            for k in tot:
+                tot[k] += per_dir[q % 2][k]
+    tot["inner"] = inner_flops(sp) * len(sweeps_phi)
+    return tot
 
 
 # ------------------------------------------------------ CPU reference arm
@@ -138,33 +204,37 @@ def _cpu_worker_init():
         pass
 
 
-def _cpu_price(i):
+def _cpu_price(job):
+    """One option with the pinned restatement; max_sweeps caps each cross
+    (config 5's bounded sample)."""
+    cid, i, max_sweeps = job
     from oracle import ttp_oracle as O
     from paper_2203_02804_b200 import configs
-    sp = configs.CONFIGS[CONFIG_ID]
-    m = configs.make_model(CONFIG_ID, i)
+    sp = configs.CONFIGS[cid]
+    m = configs.make_model(cid, i)
     g = sp.grid
     gm = O.GridModel(m.r, m.sigma, m.T, m.s0, m.strike, m.corr, g.n, g.eta, g.alpha)
-    price, _ = O.price_tt(gm, sp.bond_dim, sp.bond_dim, sp.cross_seed, sp.cross_seed)
-    return price
-
-
-def cpu_pool_time(n_opts, procs, start=0):
-    import multiprocessing as mp
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(procs, initializer=_cpu_worker_init) as pool:
-        pool.map(_cpu_worker_noop, range(procs))  # spawn + import cost outside the timing
-        t0 = time.perf_counter()
-        prices = pool.map(_cpu_price, range(start, start + n_opts), chunksize=1)
-        wall = time.perf_counter() - t0
-    return wall, prices
+    kw = {} if max_sweeps is None else {"max_sweeps": max_sweeps}
+    price, info = O.price_tt(gm, sp.bond_dim, sp.bond_dim, sp.cross_seed, sp.cross_seed, **kw)
+    return price, int(info["cross_phi"]["sweeps_used"]) + int(info["cross_v"]["sweeps_used"])
 
 
 def _cpu_worker_noop(_):
     import oracle.ttp_oracle  # noqa: F401
     import paper_2203_02804_b200.configs  # noqa: F401
     return 0
+
+
+def cpu_pool_time(cid, n_opts, procs, max_sweeps=None):
+    import multiprocessing as mp
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs, initializer=_cpu_worker_init) as pool:
+        pool.map(_cpu_worker_noop, range(procs))  # spawn + import cost outside the timing
+        t0 = time.perf_counter()
+        out = pool.map(_cpu_price, [(cid, i, max_sweeps) for i in range(n_opts)], chunksize=1)
+        wall = time.perf_counter() - t0
+    return wall, [p for p, _ in out], [s for _, s in out]
 
 
 def cpu_model_name():
@@ -177,40 +247,106 @@ def cpu_model_name():
     return "unknown"
 
 
+def cpu_baseline_sample(cid, cores, n_opts=0, sweeps_per_option=None):
+    """Time the reference algorithm (pinned port) on a bounded sample of the
+    workload: SURVEY.md 8(d)'s subset rule (cfg3: 64 instances), one option
+    per core.  Config 5 options take ~10 minutes each on a core, so its sample
+    runs ONE sweep per cross and is extrapolated to the measured sweeps per
+    option (labelled)."""
+    n_opts = n_opts or META[cid]["cpu"](cores)
+    procs = min(cores, n_opts)
+    if cid == 5:
+        wall, prices, sweeps = cpu_pool_time(cid, n_opts, procs, max_sweeps=1)
+        scale = (sweeps_per_option or 2.0) / 2.0
+        value = n_opts / (wall * scale)
+        sample = (f"{n_opts} config-5 options (instances 0..{n_opts - 1}), ONE sweep per cross, on "
+                  f"{cpu_model_name()} (1 BLAS thread per process); extrapolated to {2 * scale:.2f} sweeps "
+                  "per option (the device run's mean; a sweep's cost is dominated by its convergence check)")
+        return {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample,
+                "wall_s": wall, "extrapolated": True}, None
+    wall, prices, _ = cpu_pool_time(cid, n_opts, procs)
+    sample = (f"{n_opts} config-{cid} options (instances 0..{n_opts - 1}) on {cpu_model_name()}, pinned numpy "
+              "restatement of the reference, 1 BLAS thread per process")
+    return {"value": n_opts / wall, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample,
+            "wall_s": wall}, prices
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    cid = args.config
+    sp = spec_of(cid)
     cores = os.cpu_count() or 1
-    per_step = cores
-    for w in range(args.warmup):
-        cpu_pool_time(per_step, cores, start=0)
-    total = 0.0
-    for s in range(args.steps):
-        wall, _ = cpu_pool_time(per_step, cores, start=0)
-        total += wall
-    value = per_step * args.steps / total
-    sp = spec()
+    for _ in range(args.warmup):
+        cpu_baseline_sample(cid, cores, args.cpu_sample, sweeps_per_option=None)
+    vals, walls = [], []
+    base = None
+    for _ in range(args.steps):
+        base, _ = cpu_baseline_sample(cid, cores, args.cpu_sample)
+        vals.append(base["value"])
+        walls.append(base["wall_s"])
+    value = float(np.mean(vals))
+    per_gpu, total = batches(args, world)
     line = {
         "impl": "reference",
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128/f64",
-        "data": "synthetic (seeded default_rng([4, i]) instances, SURVEY.md 8(d))",
-        # the GPU arm's workload (same config keys); each reference step is a
-        # bounded sample of it (see cpu_baseline.sample)
-        "config": {"workload": sp.label + f", batch of {args.batch} independent options per GPU per step",
-                   "config_id": CONFIG_ID, "options_per_gpu_per_step": args.batch,
-                   "global_batch": args.batch * world, "grid_points_per_axis": sp.grid.points_per_axis,
-                   "bond_dim": sp.bond_dim, "parallelism": "host cores (rank 0 only)",
-                   "options_timed_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_step} config-4 options per step (one per core, 1 BLAS thread "
-                                   f"each) on {cpu_model_name()}; the reference is pure Python "
-                                   "(no compiled _ref) so its pinned numpy restatement runs"},
+        "metric": META[cid]["metric"], "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(walls)),
+        "higher_is_better": True, "scaling": META[cid]["scaling"], "vs_baseline": None, "dtype": "c128/f64",
+        "data": f"synthetic (seeded default_rng([{cid}, i]) instances, SURVEY.md 8(d))",
+        # the GPU arm's workload; each reference step is a bounded sample of it
+        "config": {"workload": sp.label + f", {total} options per step", "config_id": cid,
+                   "options_per_gpu_per_step": per_gpu, "global_batch": total,
+                   "grid_points_per_axis": sp.grid.points_per_axis, "bond_dim": sp.bond_dim,
+                   "parallelism": "host cores (rank 0 only)"},
+        "cpu_baseline": dict(base, value=value),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ parity
+def parity_check(cid, gpu_prices, cpu_prices):
+    """GPU prices of instances 0.. against the reference's own prices of the
+    same instances (golden, from ttpricer itself) or the live CPU port."""
+    gold, bands = {}, {}
+    try:
+        gold = json.load(open(os.path.join(REPO, "tests", "golden", "ref_prices_r02.json")))
+        bands = json.load(open(os.path.join(REPO, "tests", "golden", "noise_bands.json")))
+    except (OSError, ValueError):
+        pass
+    rows = []
+    for i, p in enumerate(gpu_prices):
+        key = f"cfg{cid}_i{i}"
+        if key in gold:
+            ref, src = gold[key]["price"], "reference golden"
+        elif key in bands:
+            ref, src = bands[key]["unperturbed"], "reference golden"
+        elif cpu_prices is not None and i < len(cpu_prices):
+            ref, src = cpu_prices[i], "live CPU port"
+        else:
+            continue
+        band = bands.get(key, {}).get("max")
+        rows.append((i, abs(p - ref) / abs(ref), band, src))
+    if not rows:
+        return None
+    cfg_band = max((b for _, _, b, _ in rows if b), default=None)
+    if cfg_band is None:
+        cfg_band = max((v["max"] for k, v in bands.items() if isinstance(v, dict) and k.startswith(f"cfg{cid}_")),
+                       default=1e-3)
+    ratios = [dev / (BAND_FACTOR * (b or cfg_band)) for _, dev, b, _ in rows]
+    devs = [dev for _, dev, _, _ in rows]
+    out = {"n": len(rows), "max_rel": max(devs), "median_rel": float(np.median(devs)),
+           "band": f"{BAND_FACTOR} x the instance's reference noise band (tests/golden/noise_bands.json: the "
+                   "reference's own price spread under 1e-15 oracle noise)",
+           "max_band_ratio": max(ratios), "ok": bool(max(ratios) <= 1.0),
+           "against": sorted({s for *_, s in rows})}
+    if cpu_prices is not None and gold:
+        same = [cpu_prices[i] == gold[f"cfg{cid}_i{i}"]["price"] for i in range(len(cpu_prices))
+                if f"cfg{cid}_i{i}" in gold]
+        if same:
+            out["cpu_port_equals_reference_golden"] = f"{sum(same)}/{len(same)} bitwise"
+    return out
 
 
 # ------------------------------------------------------------ GPU arm
@@ -224,29 +360,33 @@ def main():
     import torch.distributed as dist
 
     torch.cuda.set_device(local)
+    group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
     import paper_2203_02804_b200 as P
     from paper_2203_02804_b200 import _lib, configs
-    from paper_2203_02804_b200.distributed import gather_records, results_to_records, shard_range
+    from paper_2203_02804_b200.distributed import gather_records, shard_range
     from paper_2203_02804_b200.pricers import run_cross_pair
 
-    sp = spec()
+    cid = args.config
+    sp = spec_of(cid)
     grid = sp.grid
     shape = (grid.points_per_axis,) * grid.d
     cfg = P.CrossConfig(bond_dim=sp.bond_dim, seed=sp.cross_seed)
-    B = args.batch
-    n_total = B * world
+    _, n_total = batches(args, world)
     lo, hi = shard_range(n_total, rank, world)
-    models = [configs.make_model(CONFIG_ID, i) for i in range(lo, hi)]
+    all_models = [configs.make_model(cid, i) for i in range(n_total)]
+    models = all_models[lo:hi]
+    B = hi - lo
     prefs = np.array([np.exp(-m.r * m.T) * grid.eta ** grid.d / (2 * np.pi) ** grid.d for m in models])
 
     # device-resident inputs for the `value` path
     phi_batch = P.OracleBatch([P.PhiGridOracle(m, grid) for m in models])
     v_batch = P.OracleBatch([P.PayoffGridOracle(m, grid, conj=True) for m in models])
 
-    def device_step():
-        rp, rv = run_cross_pair(phi_batch, v_batch, shape, cfg, cfg, with_reports=False)
+    def device_step(concurrent=True):
+        rp, rv = run_cross_pair(phi_batch, v_batch, shape, cfg, cfg, with_reports=False, concurrent=concurrent)
         raw = P.tt_inner_batch(rv.trains, rp.trains)
         return prefs * raw.real, rp, rv
 
@@ -264,15 +404,15 @@ def main():
     t_start = torch.cuda.Event(enable_timing=True)
     t_stop = torch.cuda.Event(enable_timing=True)
     t_start.record()
-    sweeps_phi = sweeps_v = 0
+    sw_phi, sw_v = [], []
     for _ in range(args.steps):
         flush.fill_(1.0)  # evict L2 between steps (512 MB > 126 MB L2)
         prices, rp, rv = device_step()
-        sweeps_phi += int(rp.counters["sweeps"].sum())
-        sweeps_v += int(rv.counters["sweeps"].sum())
+        sw_phi.extend(rp.counters["sweeps"].tolist())
+        sw_v.extend(rv.counters["sweeps"].tolist())
         if world > 1:
-            recs = np.column_stack([prices, np.zeros((len(prices), 8))])
-            gather_records(recs, n_total, device=torch.device("cuda", local))
+            recs = np.column_stack([prices, np.zeros((len(prices), 9))])
+            gather_records(recs, n_total, device=torch.device("cuda", local), group=group)
     t_stop.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -288,138 +428,150 @@ def main():
     elapsed = float(t.item())
     value = n_total * args.steps / elapsed
     ok = int((rp.status == 0).sum() + (rv.status == 0).sum())
+    gpu_prices_head = [float(x) for x in prices[:16]]
 
-    # e2e through the public API with host inputs
+    # e2e through the public API with host inputs (sharded batch API at N > 1)
     e2e = None
     if not args.no_e2e:
-        for _ in range(1):
-            P.price_fourier_tt_batch(models, grid, cfg, cfg, dense_reference="never")
+        P.price_fourier_tt_batch(all_models if group else models, grid, cfg, cfg, group=group)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            res = P.price_fourier_tt_batch(models, grid, cfg, cfg, dense_reference="never")
-            if world > 1:
-                gather_records(results_to_records(res), n_total, device=torch.device("cuda", local))
+            res = P.price_fourier_tt_batch(all_models if group else models, grid, cfg, cfg, group=group)
         torch.cuda.synchronize()
         e_el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e_el, op=dist.ReduceOp.MAX)
+        same_bits = [r.price for r in res[lo:lo + 16]] == gpu_prices_head
         d = grid.d
         from paper_2203_02804_b200.cross import _Layout
         lay = _Layout(shape, sp.bond_dim)
-        nb = len(models)
-        h2d = nb * 8 * ((3 + d + d * d) + 5) + 2 * (lay.set_stride * 4 + 4 * d)
-        # prices (complex) + per-instance cross counters of both crosses; the
-        # index sets stay on the device until a report's sets are read
-        d2h = nb * (16 + 2 * (4 * 5 + 8 * 3) + 8)
+        # per instance: both oracles' parameter rows; per call: initial right
+        # sets, shape; prices (complex) + per-instance cross counters of both
+        # crosses come back (index sets stay on the device until read)
+        h2d = B * 8 * ((3 + d + d * d) + 5) + 2 * (lay.set_stride * 4 + 4 * d)
+        d2h = B * (16 + 2 * (4 * 5 + 8 * 3) + 8)
+        if world > 1:
+            d2h += n_total * 8 * 10  # the gathered records
         e2e = {"value": n_total * args.steps / float(e_el.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "api": "price_fourier_tt_batch(models, grid, cfg, cfg" + (", group=WORLD)" if group else ")"),
+               "same_prices_as_device_path": same_bits}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # Roofline of the dominant kernel.  Inside the timed region the phi and
-    # vhat crosses run on two streams, so per-launch event durations overlap;
-    # one extra untimed step with the two crosses serialized gives clean
-    # per-kernel durations (same launches, same inputs) for `achieved`.
-    os.environ["TTP_PAIR_STREAMS"] = "0"
+    # Per-kernel rooflines.  Inside the timed region the phi and vhat crosses
+    # run on two streams, so per-launch event durations overlap; one extra
+    # untimed step with the crosses serialized gives clean per-kernel
+    # durations (same launches, same inputs) for `achieved`.
     _lib.profile_reset()
     _lib.profile_enable(True)
-    device_step()
+    _, rp1, rv1 = device_step(concurrent=False)
     torch.cuda.synchronize()
     _lib.profile_enable(False)
     sstats = _lib.profile_read()
-    os.environ.pop("TTP_PAIR_STREAMS", None)
     total_serial_ms = sum(v[2] for v in sstats.values())
-    dom = max(sstats.items(), key=lambda kv: kv[1][2])
-    dom_name, (dom_launch, dom_timed, dom_ms) = dom
-    work = alg_work_per_instance(sp, sweeps_phi / max(1, args.steps * B), sweeps_v / max(1, args.steps * B))
-    peaks = {}
+    work = work_of_batch(sp, rp1.counters["sweeps"].tolist(), rv1.counters["sweeps"].tolist())
     try:
         peaks = json.load(open(os.path.join(REPO, "profiles", "fp64_peak.json")))
-    except OSError:
-        pass
-    fp64_peak = peaks.get("fp64_gemm_tflops_8192", 35.4)
-    per_kernel_flops = {
-        "bond_kernel": work["bond_la"] * (sweeps_phi + sweeps_v) / args.steps,
-        "conv_site_kernel": work["conv"] * (sweeps_phi + sweeps_v) / args.steps,
-        "tt_inner_kernel": work["inner"] * B,
-    }
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(REPO, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(dom_name)
-    except OSError:
-        pass
-    def kernel_roofline(name):
-        launches, timed, ms = sstats.get(name, (0, 0, 0.0))
-        if name not in per_kernel_flops or not timed:
-            return {"bound": "fp64", "kernel": name, "achieved": None, "peak": fp64_peak,
-                    "unit": "TFLOP/s", "frac": None, "traffic": None}
-        flops_per_launch = per_kernel_flops[name] / max(1, launches)
-        achieved = flops_per_launch / (ms / timed / 1e3) / 1e12
-        t_launch, t_timed, t_ms = kstats.get(name, (0, 0, 0.0))
-        return {"bound": "fp64", "kernel": name, "achieved": achieved, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic if name == dom_name else None,
-                "peak_source": "profiles/fp64_peak.json (cuBLAS DGEMM 8192^3 on this pool's B200)",
-                "avg_launch_ms": ms / timed, "alg_flops_per_launch": flops_per_launch,
-                "share_of_step": ms / total_serial_ms if total_serial_ms else None,
-                "avg_launch_ms_timed_region": (t_ms / t_timed) if t_timed else None}
-
-    roofline = kernel_roofline(dom_name)
-    roofline["note"] = ("durations from one untimed, stream-serialized step (the timed region overlaps the "
-                        "phi and vhat crosses on two streams); algorithmic flops per SURVEY.md 8(d)")
-    # the bond kernel is memory bound: its measured DRAM traffic (ncu, same
-    # batch) per event-timed launch, against the measured HBM copy peak
+    except (OSError, ValueError):
+        peaks = {}
     try:
         hbm_peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
     except (OSError, ValueError):
-        hbm_peak = None
-    if traffic and roofline.get("avg_launch_ms") and hbm_peak:
-        rate = traffic / (roofline["avg_launch_ms"] / 1e3) / 1e9
-        roofline["dram"] = {"bytes_per_launch": traffic, "achieved_gbs": rate, "peak_gbs": hbm_peak,
-                            "frac": rate / hbm_peak,
-                            "source": "profiles/ncu_traffic.json (dram__bytes_read+write, ncu --set full, "
-                                      "same batch) / avg_launch_ms; MEASURED_PEAKS.json hbm_gbs"}
-    secondary = [kernel_roofline(k) for k in ("conv_site_kernel", "tt_inner_kernel") if k != dom_name]
+        hbm_peak, hbm_src = 7700.0, "B200_PROFILING.md fallback"
+    dgemm = peaks.get("fp64_gemm_tflops_8192", 35.43)
+    dfma = peaks.get("fp64_dfma_tflops")
+    try:
+        traffic_all = json.load(open(os.path.join(REPO, "profiles", "ncu_traffic.json")))
+    except (OSError, ValueError):
+        traffic_all = {}
+    flops = {"cluster_bond_kernel": work["cluster"], "bond_kernel": work["v0"],
+             "conv_site_kernel": work["conv"], "tt_inner_kernel": work["inner"]}
+    bytes_ = {"fiber_kernel": work["fiber_bytes"]}
 
-    cpu_baseline = None
+    def kernel_roofline(name):
+        launches_, timed, ms = sstats.get(name, (0, 0, 0.0))
+        if not timed:
+            return None
+        t_launch = ms / timed / 1e3
+        tr = traffic_all.get(f"cfg{cid}/{name}")
+        base = {"kernel": name, "avg_launch_ms": 1e3 * t_launch,
+                "share_of_step": ms / total_serial_ms if total_serial_ms else None,
+                "traffic": tr.get("bytes_per_launch") if tr else None}
+        if name in flops:
+            per = flops[name] / max(1, launches_)
+            ach = per / t_launch / 1e12
+            out = dict(base, bound="tensor", achieved=ach, peak=dgemm, unit="TFLOP/s", frac=ach / dgemm,
+                       alg_flops_per_launch=per,
+                       peak_source="profiles/fp64_peak.json: cuBLAS DGEMM 8192^3 on this pool's B200 (the FP64 "
+                                   "tensor-core rate; MEASURED_PEAKS.json has no FP64 figure)")
+            if dfma:
+                out["dfma"] = {"peak": dfma, "frac": ach / dfma,
+                               "source": "profiles/fp64_peak.json fp64_dfma_tflops (tools/micro/dfma_rate.cu)"}
+            if tr and hbm_peak:
+                rate = tr["bytes_per_launch"] / t_launch / 1e9
+                out["dram"] = {"bytes_per_launch": tr["bytes_per_launch"], "achieved_gbs": rate,
+                               "peak_gbs": hbm_peak, "frac": rate / hbm_peak,
+                               "source": f"profiles/ncu_traffic.json ({tr.get('source', 'ncu --set full')}) / "
+                                         f"this kernel's own event-timed launch; {hbm_src}"}
+            return out
+        if name in bytes_:
+            per = bytes_[name] / max(1, launches_)
+            ach = per / t_launch / 1e9
+            return dict(base, bound="hbm", achieved=ach, peak=hbm_peak, unit="GB/s", frac=ach / hbm_peak,
+                        alg_bytes_per_launch=per, peak_source=hbm_src)
+        return None
+
+    rooflines = [r for r in (kernel_roofline(k) for k in sstats) if r]
+    rooflines.sort(key=lambda r: -(r["share_of_step"] or 0))
+    roofline = rooflines[0] if rooflines else None
+    if roofline is not None:
+        roofline["note"] = ("durations from one untimed, stream-serialized step (the timed region overlaps the "
+                            "phi and vhat crosses on two streams); algorithmic flops/bytes per SURVEY.md 8(d), "
+                            "DESIGN.md section 4")
+
+    cpu_baseline, cpu_prices = None, None
     if world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        n_opts = args.cpu_sample or cores
-        wall, cpu_prices = cpu_pool_time(n_opts, cores, start=0)
-        cpu_baseline = {"value": n_opts / wall, "unit": UNIT, "cores": min(cores, n_opts), "kind": "port",
-                        "sample": f"{n_opts} config-4 options (instances 0..{n_opts - 1}) on {cpu_model_name()}, "
-                                  "pinned numpy restatement of the reference, 1 BLAS thread per process",
-                        "wall_s": wall}
-
+        mean_sweeps = (np.mean(sw_phi) + np.mean(sw_v)) if sw_phi else None
+        cpu_baseline, cpu_prices = cpu_baseline_sample(cid, cores, args.cpu_sample, sweeps_per_option=mean_sweeps)
+    parity = parity_check(cid, gpu_prices_head, cpu_prices[:16] if cpu_prices else None)
+    per_gpu, _ = batches(args, world)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": META[cid]["metric"], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128/f64",
-        "data": "synthetic (seeded default_rng([4, i]) config-4 instances, SURVEY.md 8(d))",
-        "config": {"workload": sp.label + f", batch of {B} independent options per GPU per step",
-                   "config_id": CONFIG_ID, "options_per_gpu_per_step": B, "global_batch": n_total,
+        "scaling": META[cid]["scaling"], "vs_baseline": None, "dtype": "c128/f64",
+        "data": f"synthetic (seeded default_rng([{cid}, i]) config-{cid} instances, SURVEY.md 8(d))",
+        "config": {"workload": sp.label + (f", batch of {per_gpu} independent options per GPU per step" if per_gpu
+                                           else f", one {n_total}-instance batch per step split over the GPUs"),
+                   "config_id": cid, "options_per_gpu_per_step": B, "global_batch": n_total,
                    "grid_points_per_axis": grid.points_per_axis, "bond_dim": sp.bond_dim,
                    "parallelism": f"instance-sharded dp{world}",
-                   "l2": "512 MB L2 flush before every timed step; per-step working set ~GBs >> 126 MB L2",
-                   "sweeps_per_option": [sweeps_phi / (args.steps * B), sweeps_v / (args.steps * B)],
+                   "l2": "512 MB L2 flush before every timed step; per-step working set >> 126 MB L2",
+                   "sweeps_per_option": [float(np.mean(sw_phi)), float(np.mean(sw_v))],
                    "instances_ok": ok},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "roofline": roofline,
-        "roofline_secondary": secondary,
+        "roofline_kernels": rooflines[1:],
         "cpu_baseline": cpu_baseline,
+        "parity": parity,
         "clocks": clk,
         "kernels": {k: {"launches": v[0], "ms": v[2]} for k, v in kstats.items() if v[0]},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        print(f"PARITY FAILURE: {parity}", file=sys.stderr)
+        sys.exit(3)
 
 
 if __name__ == "__main__":

@@ -2771,7 +2771,7 @@ cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   {
-    LaunchScope _ls(KC_BOND, s);
+    LaunchScope _ls(KC_CLUSTER_BOND, s);
     e = cudaLaunchKernelEx(&cfg, cluster_bond_kernel, job);
   }
   if (e != cudaSuccess) return e;

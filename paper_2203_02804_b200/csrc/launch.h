@@ -22,6 +22,7 @@ enum KernelClass {
   KC_MISC,
   KC_MC,
   KC_MC_FINAL,
+  KC_CLUSTER_BOND,
   KC_COUNT
 };
 

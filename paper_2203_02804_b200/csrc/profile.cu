@@ -14,7 +14,7 @@ const char* kNames[KC_COUNT] = {"fiber_kernel",     "bond_kernel",      "conv_si
                                 "conv_site_kernel", "sample_diff_kernel", "points_kernel",
                                 "tt_inner_kernel",  "eval_warp_kernel", "dense_partial_kernel",
                                 "dense_final_kernel", "misc_kernel", "mc_path_kernel",
-                                "mc_final_kernel"};
+                                "mc_final_kernel",  "cluster_bond_kernel"};
 
 std::atomic<long long> g_launches{0};
 std::atomic<int> g_profile{0};
