@@ -156,8 +156,9 @@ def sweep_work(sp, direction):
     """Algorithmic work of one directional sweep of one cross:
     bond linear algebra 44 m r^2 flops per bond, split by the kernel that runs
     it (blocks >= 1 MB: cluster kernel, else the one-CTA kernel, as
-    driver.cu:run_bond decides), fiber bytes (16 per sampled entry, the last
-    core included), convergence check 8 M sum r_k r_k+1 flops."""
+    driver.cu:run_bond decides), fiber-kernel bytes (16 per entry it writes:
+    the one-CTA path's blocks and the edge core), convergence check
+    8 M sum r_k r_k+1 flops."""
     from paper_2203_02804_b200.cross import rank_profile
     d, n = sp.d, sp.grid.points_per_axis
     r = rank_profile((n,) * d, sp.bond_dim)
@@ -166,11 +167,11 @@ def sweep_work(sp, direction):
     for m, rk in block_shapes(sp, direction):
         f = 44.0 * m * rk * rk
         if m * rk * 16 >= (1 << 20):
-            cluster += f
+            cluster += f  # the cluster kernel evaluates its own fibers (load_block)
         else:
             v0 += f
-        entries += m * rk
-    entries += (r[d - 1] * n) if direction == 0 else (n * r[1])
+            entries += m * rk  # fiber kernel, then the one-CTA bond kernel
+    entries += (r[d - 1] * n) if direction == 0 else (n * r[1])  # the edge core
     conv = 8.0 * 50_000 * sum(r[k] * r[k + 1] for k in range(1, d))
     return {"cluster": cluster, "v0": v0, "fiber_bytes": 16.0 * entries, "conv": conv}
 
@@ -381,14 +382,29 @@ def main():
     B = hi - lo
     prefs = np.array([np.exp(-m.r * m.T) * grid.eta ** grid.d / (2 * np.pi) ** grid.d for m in models])
 
-    # device-resident inputs for the `value` path
-    phi_batch = P.OracleBatch([P.PhiGridOracle(m, grid) for m in models])
-    v_batch = P.OracleBatch([P.PayoffGridOracle(m, grid, conj=True) for m in models])
+    # device-resident inputs for the `value` path, in chunks that fit device
+    # memory (cfg3's 4096 instances; the public API chunks the same way)
+    from paper_2203_02804_b200.pricers import max_batch
+    chunk = max_batch(shape, cfg, cfg, n=B)
+    chunks = []
+    for c0 in range(0, B, chunk):
+        ms = models[c0:c0 + chunk]
+        chunks.append((P.OracleBatch([P.PhiGridOracle(m, grid) for m in ms]),
+                       P.OracleBatch([P.PayoffGridOracle(m, grid, conj=True) for m in ms])))
+
+    class _Sweeps:  # per-instance sweep counts and statuses of one step
+        def __init__(self, parts):
+            self.counters = {"sweeps": np.concatenate([p.counters["sweeps"] for p in parts])}
+            self.status = np.concatenate([p.status for p in parts])
 
     def device_step(concurrent=True):
-        rp, rv = run_cross_pair(phi_batch, v_batch, shape, cfg, cfg, with_reports=False, concurrent=concurrent)
-        raw = P.tt_inner_batch(rv.trains, rp.trains)
-        return prefs * raw.real, rp, rv
+        raws, rps, rvs = [], [], []
+        for phi_batch, v_batch in chunks:
+            rp, rv = run_cross_pair(phi_batch, v_batch, shape, cfg, cfg, with_reports=False, concurrent=concurrent)
+            raws.append(P.tt_inner_batch(rv.trains, rp.trains))
+            rps.append(rp)
+            rvs.append(rv)
+        return prefs * np.concatenate(raws).real, _Sweeps(rps), _Sweeps(rvs)
 
     for _ in range(args.warmup):
         prices, rp, rv = device_step()
@@ -554,6 +570,7 @@ def main():
                    "config_id": cid, "options_per_gpu_per_step": B, "global_batch": n_total,
                    "grid_points_per_axis": grid.points_per_axis, "bond_dim": sp.bond_dim,
                    "parallelism": f"instance-sharded dp{world}",
+                   "device_chunks": len(chunks),
                    "l2": "512 MB L2 flush before every timed step; per-step working set >> 126 MB L2",
                    "sweeps_per_option": [float(np.mean(sw_phi)), float(np.mean(sw_v))],
                    "instances_ok": ok},

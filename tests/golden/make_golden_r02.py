@@ -125,6 +125,21 @@ def gen_prices():
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+def gen_prices5():
+    """Config 5 (d=20, 257 points, D=64): the reference needs ~10 minutes per
+    option on one core; instances 0-7 (SURVEY.md 8(d)'s subset rule) ->
+    ref_prices_cfg5.json."""
+    jobs = [(5, i) for i in range(8)]
+    out = {}
+    with ProcessPoolExecutor(max_workers=min(8, os.cpu_count())) as ex:
+        for (cid, inst), rec in ex.map(_price, jobs):
+            out[f"cfg{cid}_i{inst}"] = rec
+            print(f"cfg{cid} i{inst}: {rec['price']!r} ({rec['wall_s']:.1f} s)", flush=True)
+    out["generator"] = "tests/golden/make_golden_r02.py prices5: ttpricer.price_fourier_tt(dense_reference='never'), 1 BLAS thread"
+    with open(os.path.join(HERE, "ref_prices_cfg5.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
 def tt32_target():
     """Seeded rank-32 train on (129,)^10, cores scaled so entries stay O(1)."""
     rng = np.random.default_rng(2032)

@@ -1,6 +1,6 @@
 """Summarise a round's ncu artefacts into profiles/ (dev tool, runs here).
 
-usage: python tools/ncu_summary.py <prof dir> <round tag> [--no-traffic]
+usage: python tools/ncu_summary.py <prof dir> <round tag> [--config=N] [--no-traffic]
   * launch list (gpu__time_duration per launch) -> per-kernel totals/shares
   * each .ncu-rep -> key metrics (duration, DRAM bytes, pipe utilisation,
     occupancy, stall reasons) and profiles/ncu_traffic.json (DRAM bytes per
@@ -15,6 +15,7 @@ import sys
 from collections import defaultdict
 
 src, tag = sys.argv[1], sys.argv[2]
+CFG = next((a.split("=", 1)[1] for a in sys.argv[3:] if a.startswith("--config=")), "4")
 dst = os.path.join("profiles", tag)
 os.makedirs(dst, exist_ok=True)
 
@@ -85,11 +86,13 @@ for rep in sorted(glob.glob(os.path.join(src, "*.ncu-rep"))):
         val = float(val.replace(",", ""))
         return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
     if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
-        # keyed by bench.py's kernel classes (csrc/launch.h KernelClass names)
+        # keyed "cfg<id>/<bench kernel class>" (csrc/launch.h KernelClass names)
         short = kname.split("::")[-1].split("<")[0]
-        short = {"cluster_bond_kernel": "bond_kernel", "bond_kernel": "bond_kernel",
-                 "conv_site_dmma_kernel": "conv_site_kernel", "tt_inner_staged_kernel": "tt_inner_kernel"}.get(short, short)
-        traffic[short] = tobytes(d["dram__bytes_read.sum"]) + tobytes(d["dram__bytes_write.sum"])
+        short = {"conv_site_dmma_kernel": "conv_site_kernel", "tt_inner_chunk_kernel": "tt_inner_kernel",
+                 "tt_inner_split_kernel": "tt_inner_kernel"}.get(short, short)
+        traffic[f"cfg{CFG}/{short}"] = {
+            "bytes_per_launch": tobytes(d["dram__bytes_read.sum"]) + tobytes(d["dram__bytes_write.sum"]),
+            "source": f"ncu --set full, {os.path.basename(rep)} ({tag}): dram__bytes_read.sum + dram__bytes_write.sum"}
     print(json.dumps(summ, indent=1))
 if "--no-traffic" not in sys.argv[3:]:  # secondary captures at other configs leave the bench's traffic alone
     json.dump(traffic, open(traffic_path, "w"), indent=1)

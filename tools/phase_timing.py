@@ -1,7 +1,11 @@
-"""Per-phase clock64 marks of the cluster bond kernel (dev tool)."""
+"""Per-phase clock64 marks of the cluster bond kernel (dev tool; the phase
+clocks exist only in the -DTTP_DEV library, so this loads it)."""
 import ctypes
+import os
 import sys
 import time
+
+os.environ["TTP_DEV_LIBRARY"] = "1"
 
 import numpy as np
 import torch
@@ -20,7 +24,7 @@ for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
     ob = P.OracleBatch([P.PhiGridOracle(m, spec.grid) for m in models])
     P.tt_cross_batch(ob, shape, cfg, with_reports=False)
     torch.cuda.synchronize()
-    lib.ttp_debug_phase_clocks(1, None, 0)
+    lib.ttp_dev_phase_clocks(1, None, 0)
     out = (ctypes.c_int64 * 32)()
     _lib.profile_reset(); _lib.profile_enable(True)
     t0 = time.perf_counter()
@@ -29,15 +33,15 @@ for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
     wall = time.perf_counter() - t0
     _lib.profile_enable(False)
     st = _lib.profile_read()
-    lib.ttp_debug_phase_clocks(0, out, 32)
+    lib.ttp_dev_phase_clocks(0, out, 32)
     clk = [out[i] for i in range(9)]
     ghz = 1.965
     marks = []
     for k in range(1, 9):
         if clk[k] and clk[k - 1] and clk[k] >= clk[0]:
             marks.append(f"{names[k]}={(clk[k] - clk[k - 1]) / ghz / 1e3:.1f}us")
-    print(f"cfg{cid} batch {nb}: wall {wall * 1e3:.1f} ms; bond kernel {st['bond_kernel'][2]:.2f} ms / "
-          f"{st['bond_kernel'][0]} launches; conv {st['conv_site_kernel'][2]:.2f} ms; last bond phases: "
+    print(f"cfg{cid} batch {nb}: wall {wall * 1e3:.1f} ms; bond kernel {st['cluster_bond_kernel'][2] + st['bond_kernel'][2]:.2f} ms / "
+          f"{st['cluster_bond_kernel'][0] + st['bond_kernel'][0]} launches; conv {st['conv_site_kernel'][2]:.2f} ms; last bond phases: "
           + " ".join(marks) + f"; total {(clk[8] - clk[0]) / ghz / 1e3:.1f}us", flush=True)
     sub = ["pivot+recomp", "partials", "clsync", "reduce", "update", "wy.gram", "wy.exchange"]
     print("    colbasis sub-phases (all bonds of the sweep): " + " ".join(
