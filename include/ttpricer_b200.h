@@ -237,6 +237,18 @@ int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const double* d_mats, 
                int64_t max_iters, double rank_tol, int64_t* h_sel, int32_t* h_status,
                void* d_ws, size_t ws_bytes, void* stream);
 
+/* _column_basis (cross.py:103-119: scipy.linalg.qr(pivoting=True), the rank
+ * check of lines 110-118) on n_mat (rows x cols) complex matrices, row-major
+ * like numpy, exactly as the bond kernel's global-slice path computes it
+ * (TSQR + zlaqp2 on the triangle for 17 <= cols <= 32).  d_q receives n_mat
+ * column-major (rows x cols) orthonormal bases, columns in pivot order
+ * (the reference's Q up to unimodular column phases).  The shapes that path
+ * serves: rows >= 2 cols, cols <= 64, rows * cols * 16 >= 1 MiB. */
+size_t ttp_column_basis_workspace(int32_t n_mat, int64_t rows, int32_t cols);
+int ttp_column_basis(int32_t n_mat, int64_t rows, int32_t cols, const double* d_mats,
+                     double rank_tol, double* d_q, int32_t* h_status, void* d_ws,
+                     size_t ws_bytes, void* stream);
+
 /* One-call batch pricing (price_fourier_tt, pricers.py:256-294, for n_inst
  * options sharing grid and configs): the phi cross (PHI_GBM oracle), the
  * vhat cross (VHAT_MIN oracle, conj_flag 1), the bra-conjugated inner

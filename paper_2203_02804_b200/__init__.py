@@ -42,7 +42,7 @@ from .tensor_train import (
     tt_rand_sample_diff,
     tt_save_json,
 )
-from .cross import CrossConfig, CrossReport, maxvol, tt_cross, tt_cross_batch
+from .cross import CrossConfig, CrossReport, column_basis, maxvol, tt_cross, tt_cross_batch
 from .pricers import (
     DENSE_TERM_CAP,
     GridSpec,

@@ -183,6 +183,8 @@ SIGNATURES = [
     ("ttp_price_tt_batch", _i32, [ctypes.POINTER(PriceProblem), ctypes.POINTER(CrossOut),
                                   ctypes.POINTER(CrossOut), ctypes.POINTER(_f64), ctypes.POINTER(_f64),
                                   _p, _sz, _p]),
+    ("ttp_column_basis_workspace", _sz, [_i32, _i64, _i32]),
+    ("ttp_column_basis", _i32, [_i32, _i64, _i32, _p, _f64, _p, ctypes.POINTER(_i32), _p, _sz, _p]),
     ("ttp_maxvol_workspace", _sz, [_i32, _i64, _i32]),
     ("ttp_maxvol", _i32, [_i32, _i64, _i32, _p, _f64, _i64, _f64, ctypes.POINTER(_i64),
                           ctypes.POINTER(_i32), _p, _sz, _p]),

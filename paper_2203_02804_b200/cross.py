@@ -428,6 +428,46 @@ def tt_cross(oracle, shape, cfg):
     return res.trains.to_trains()[0], res.reports[0]
 
 
+def column_basis(mats, rank_tol=0.0):
+    """Orthonormal column bases by pivoted QR, with the rank check
+    (_column_basis, cross.py:103-119), computed exactly as the bond kernel's
+    global-slice path does it (ttp_column_basis).  ``mats``: one (rows x cols)
+    matrix or a stack of them, of the shapes that path serves (rows >= 2 cols,
+    blocks of >= 1 MiB).  Returns the Q factors
+    (columns in pivot order; the reference's Q up to unimodular column
+    phases) with the stack's shape.  Raises SingularMatrixError when a matrix
+    is zero or rank deficient by ``rank_tol``."""
+    mats = np.asarray(mats, dtype=np.complex128)
+    single = mats.ndim == 2
+    if single:
+        mats = mats[None]
+    if mats.ndim != 3:
+        raise ValueError("column_basis expects a matrix or a stack of matrices")
+    n_mat, n, r = mats.shape
+    if r > MAX_BOND or n < 2 * r or n * r * 16 < (1 << 20):
+        raise ValueError(f"column_basis runs the bond kernel's global-slice path: blocks of >= 1 MiB "
+                         f"with rows >= 2 cols and cols <= {MAX_BOND}")
+    torch = _lib.require_device()
+    lib = _lib.load_library()
+    d_mat = torch.from_numpy(np.ascontiguousarray(mats)).to("cuda")
+    d_q = torch.empty((n_mat, r, n), dtype=torch.complex128, device="cuda")
+    ws_bytes = lib.ttp_column_basis_workspace(n_mat, n, r)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+    status = np.zeros(n_mat, dtype=np.int32)
+    st = lib.ttp_column_basis(n_mat, n, r, ctypes.c_void_p(d_mat.data_ptr()), float(rank_tol),
+                              ctypes.c_void_p(d_q.data_ptr()),
+                              status.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                              ctypes.c_void_p(ws.data_ptr()), ws_bytes, _lib.stream_handle())
+    _lib.raise_for(st, "column_basis")
+    if np.any(status == _lib.TTP_ERR_SINGULAR):
+        bad = int(np.argmax(status == _lib.TTP_ERR_SINGULAR))
+        raise SingularMatrixError(f"matrix {bad} of shape {(n, r)} is numerically rank deficient (or zero)")
+    for s_ in status:
+        _lib.raise_for(int(s_), "column_basis")
+    q = d_q.transpose(1, 2).cpu().numpy()
+    return q[0] if single else q
+
+
 def maxvol(mat, slack=0.01, max_iters=None, rank_tol=RANK_TOL):
     """Rows whose square submatrix has quasi-maximal volume (cross.py:208-230)."""
     mat = np.asarray(mat, dtype=np.complex128)

@@ -1,3 +1,4 @@
+#include <cstdio>
 // Host runtime of the B200 TT-Fourier pricer: the C ABI entry points and the
 // batched TT-cross sweep driver.
 //
@@ -322,6 +323,9 @@ int run_bond(const OracleDev& o, const FiberJob& f, const BondJob& bj, const Cro
     cj.wg_stride = w.mat_stride;
     const int act_tp = ck_tp::max_active_clusters(cj), act_lat = ck_lat::max_active_clusters(cj);
     const bool tp = tp_knob() >= 0 ? tp_knob() == 1 : act_tp > act_lat;
+#ifdef TTP_DEV
+    if (std::getenv("TTP_DEBUG_ACT")) std::fprintf(stderr, "run_bond m=%d r=%d act_tp=%d act_lat=%d\n", bj.m, bj.r, act_tp, act_lat);
+#endif
     if (tp && act_tp > 0) {
       TTP_CUDA_CHECK(ck_tp::launch_cluster_bond(cj, n, s));
       return TTP_OK;
@@ -719,6 +723,76 @@ extern "C" int ttp_maxvol(int32_t n_mat, int64_t rows, int32_t cols, const doubl
   return TTP_OK;
 }
 
+extern "C" size_t ttp_column_basis_workspace(int32_t n_mat, int64_t rows, int32_t cols) {
+  return ttp_maxvol_workspace(n_mat, rows, cols);
+}
+
+// _column_basis (cross.py:103-119) on n_mat (rows x cols) matrices, exactly as
+// the bond kernel's global-slice path computes it for blocks of >= 1 MB
+// (2-CTA clusters; TSQR + zlaqp2 on the triangle for 17 <= cols <= 32, the
+// restated zlaqp2 otherwise).  d_q: n_mat column-major (rows x cols) Q
+// factors, columns in pivot order.  h_status: TTP_OK or TTP_ERR_SINGULAR.
+extern "C" int ttp_column_basis(int32_t n_mat, int64_t rows, int32_t cols, const double* d_mats,
+                                double rank_tol, double* d_q, int32_t* h_status, void* d_ws,
+                                size_t ws_bytes, void* stream) {
+  if (n_mat < 0 || rows < 1 || cols < 1 || cols > 64 || rows < 2 * (int64_t)cols ||
+      rows * (int64_t)cols * (int64_t)sizeof(cplx) < (1LL << 20))
+    return ttp_fail(TTP_ERR_INVALID,
+                    "column_basis: the global-slice path serves blocks of >= 1 MiB with rows >= 2 cols, cols <= 64");
+  if (ws_bytes < ttp_column_basis_workspace(n_mat, rows, cols))
+    return ttp_fail(TTP_ERR_WORKSPACE, "column_basis: workspace too small");
+  if (n_mat == 0) return TTP_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long mr = rows * (long long)cols;
+  unsigned char* base = reinterpret_cast<unsigned char*>(d_ws);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char* p = base + off;
+    off += align_up(bytes);
+    return p;
+  };
+  BondJob bj{};
+  bj.A = (cplx*)take(sizeof(cplx) * mr * n_mat);
+  bj.W = (cplx*)take(sizeof(cplx) * mr * n_mat);
+  bj.B = (cplx*)take(sizeof(cplx) * mr * n_mat);
+  bj.iwork = (int*)take(sizeof(int) * 2 * rows * n_mat);
+  bj.dwork = (double*)take(sizeof(double) * 2 * rows * n_mat);
+  bj.sel_out = (int*)take(sizeof(int) * cols * n_mat);
+  bj.status = (int*)take(sizeof(int) * n_mat);
+  bj.m = (int)rows;
+  bj.r = cols;
+  bj.mat_stride = mr;
+  bj.iw_stride = 2 * rows;
+  bj.dw_stride = 2 * rows;
+  bj.rank_tol = rank_tol;
+  bj.max_iters = -1;
+  bj.slack = 0.01;
+  bj.sel_stride = cols;
+  bj.write_mode = 0;
+  TTP_CUDA_CHECK(cudaMemsetAsync(bj.status, 0, sizeof(int) * n_mat, s));
+  ClusterJob cj{};
+  cj.b = bj;
+  cj.cl = pow2_cluster(l2_cluster_size(), bj.m, bj.r);
+  cj.src_mode = 1;
+  cj.src = reinterpret_cast<const cplx*>(d_mats);
+  cj.src_stride = mr;
+  cj.Qg = reinterpret_cast<cplx*>(d_q);
+  cj.q_stride = mr;
+  cj.Wg = bj.W;
+  cj.Sg = bj.B;
+  cj.wg_stride = mr;
+  cj.basis_only = 1;
+  const int act_tp = ck_tp::max_active_clusters(cj), act_lat = ck_lat::max_active_clusters(cj);
+  if (act_tp > act_lat && act_tp > 0) TTP_CUDA_CHECK(ck_tp::launch_cluster_bond(cj, n_mat, s));
+  else if (act_lat > 0) TTP_CUDA_CHECK(ck_lat::launch_cluster_bond(cj, n_mat, s));
+  else return ttp_fail(TTP_ERR_INVALID, "column_basis: no cluster configuration fits");
+  std::vector<int> stat(n_mat);
+  TTP_CUDA_CHECK(cudaMemcpyAsync(stat.data(), bj.status, sizeof(int) * n_mat, cudaMemcpyDeviceToHost, s));
+  TTP_CUDA_CHECK(cudaStreamSynchronize(s));
+  for (int i = 0; i < n_mat; ++i) h_status[i] = stat[i];
+  return TTP_OK;
+}
+
 // ---------------------------------------------------------------------------
 // One-call batch pricing: phi cross, vhat cross, inner product, prefactor.
 extern "C" size_t ttp_price_tt_workspace(const ttp_price_problem* prob) {
@@ -794,6 +868,17 @@ extern "C" int ttp_dev_phase_clocks(int enable, int64_t* out, int32_t n) {
   }
   st = ck_tp::debug_phase_clocks(enable, nullptr, 0);
   if (st == TTP_OK) st = ck_lat::debug_phase_clocks(enable, nullptr, 0);
+  return st;
+}
+
+// dev: per-instance [start ns][end ns][sm] of the throughput instantiation
+extern "C" int ttp_dev_inst_times(int64_t* out, int32_t n) {
+  std::vector<int64_t> a((size_t)3 * n), b((size_t)3 * n);
+  int st = ck_tp::debug_inst_times(a.data(), n);
+  if (st == TTP_OK) st = ck_lat::debug_inst_times(b.data(), n);
+  const bool use_a = a[n] != 0;  // an end mark of instance 0
+  for (size_t i = 0; i < a.size(); ++i) out[i] = use_a ? a[i] : b[i];
+  std::fprintf(stderr, "inst times from %s\n", use_a ? "ck_tp" : "ck_lat");
   return st;
 }
 #endif

@@ -60,6 +60,8 @@ struct ClusterJob {
   int q_wy;               // form Q in compact-WY form (else zung2r rounds)
   int fused_starts;       // both dominant-row starts in one read-only pass sequence
   int fused_qr;           // column basis: each update pass also forms the next step's partials
+  int basis_only;         // stop after the column basis (ttp_column_basis)
+  int tsqr;               // global-slice mode: column basis by TSQR + zlaqp2 on the triangle (k_tsqr.cuh)
   int big;                // bit 0: per-row arrays, bit 1: B[sel,:] in global memory (set by the launcher)
   cplx* Sg;               // global-slice mode: B buffer (holds B[sel,:] in big mode), stride wg_stride
   OracleDev oracle;
@@ -77,7 +79,7 @@ struct ClusterJob {
 };
 
 #ifdef TTP_DEV
-#define TTP_DEV_CLUSTER_API int debug_phase_clocks(int enable, int64_t* out, int32_t n);
+#define TTP_DEV_CLUSTER_API int debug_phase_clocks(int enable, int64_t* out, int32_t n); int debug_inst_times(int64_t* out, int32_t n);
 #else
 #define TTP_DEV_CLUSTER_API
 #endif

@@ -69,6 +69,25 @@ __device__ int g_phase_enable;
 
 // Sub-phase cycle accumulators (cluster rank 0, thread 0 of instance 0).
 __device__ unsigned long long g_sub_clock[16];
+// Per-instance start / end (globaltimer ns) and SM of cluster rank 0.
+constexpr int INST_T_MAX = 8192;
+__device__ long long g_inst_t[3][INST_T_MAX];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define INST_MARK(k)                                                                         \
+  do {                                                                                       \
+    if (g_phase_enable && c.crank == 0 && threadIdx.x == 0 && inst < INST_T_MAX) {           \
+      g_inst_t[k][inst] = gtimer();                                                          \
+      if (k == 0) {                                                                          \
+        unsigned sm;                                                                         \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));                                      \
+        g_inst_t[2][inst] = sm;                                                              \
+      }                                                                                      \
+    }                                                                                        \
+  } while (0)
 }  // namespace
 #define SP_BEGIN(t)                                                             \
   long long t = (g_phase_enable && c.crank == 0 && threadIdx.x == 0 && blockIdx.x < (unsigned)c.C) \
@@ -83,6 +102,7 @@ __device__ unsigned long long g_sub_clock[16];
   } while (0)
 #else
 #define PHASE_MARK(k) do { } while (0)
+#define INST_MARK(k) do { } while (0)
 #define SP_BEGIN(t) do { } while (0)
 #define SP(t, k) do { } while (0)
 #endif
@@ -1351,6 +1371,8 @@ __device__ bool column_basis(cg::cluster_group& cl, CC& c, int& par, double rank
   return true;
 }
 
+#include "k_tsqr.cuh"
+
 // ------------------------------------------------------------ phase D
 // X = Q[rows]^-1 into aug's right half (every CTA, redundantly); returns
 // log|det Q[rows]|.
@@ -2445,16 +2467,20 @@ __global__ void __launch_bounds__(CT, CLUSTER_MIN_BLOCKS) cluster_bond_kernel(Cl
   const int r = c.r, m = c.m;
 
   PHASE_MARK(0);
+  INST_MARK(0);
   load_block(c, J, inst);
   PHASE_MARK(1);
   // the WY Q pass also leaves the fused starts' row norms (m > r only)
   const bool norms_in_q = J.q_wy != 0 && J.fused_starts != 0 && job.m != job.r;
-  if (!column_basis(cl, c, par, job.rank_tol, J.q_wy != 0, J.fused_qr != 0, norms_in_q)) {
+  const bool basis_ok = tsqr_usable(c, J) ? tsqr_basis(cl, c, J, inst, job.rank_tol, norms_in_q)
+                                           : column_basis(cl, c, par, job.rank_tol, J.q_wy != 0, J.fused_qr != 0, norms_in_q);
+  if (!basis_ok) {
     if (c.crank == 0 && threadIdx.x == 0) set_error(job, inst, TTP_ERR_SINGULAR);
     cl.sync();
     return;
   }
   cl.sync();  // Q rows of every CTA are now visible in global memory
+  if (J.basis_only) return;  // every CTA passed the barrier above
   if (m == r) {
     for (int t = threadIdx.x; t < r; t += CT) c.best[t] = t;
     __syncthreads();
@@ -2598,6 +2624,7 @@ __global__ void __launch_bounds__(CT, CLUSTER_MIN_BLOCKS) cluster_bond_kernel(Cl
     }
   }
   PHASE_MARK(8);
+  INST_MARK(1);
   cl.sync();  // no CTA may exit while a peer can still read its shared memory
 }
 
@@ -2696,6 +2723,16 @@ static bool fused_starts_enabled() {
   return on;
 }
 
+// TTP_TSQR=0 keeps the restated zlaqp2 column basis in global-slice mode
+// (A/B knob); default: TSQR + zlaqp2 on the triangle (k_tsqr.cuh).
+static bool tsqr_enabled() {
+  static const bool on = [] {
+    const char* e = ttp_dev_env("TTP_TSQR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // TTP_LAZY=F (1..LAZY_MAX): flush cadence of the deferred swap updates in
 // global-slice mode (1 = the eager update of every row pass); A/B knob.
 static cudaError_t apply_lazy_knob() {
@@ -2750,6 +2787,7 @@ cudaError_t launch_cluster_bond(const ClusterJob& job_in, int n_inst, cudaStream
   resolve_big(job);
   job.q_wy = q_wy_enabled() ? 1 : 0;
   job.fused_starts = fused_starts_enabled() ? 1 : 0;
+  job.tsqr = tsqr_enabled() ? 1 : 0;
   const int C = job.cl;
   const size_t smem = cluster_smem_bytes(job.b.m, job.b.r, C, job.Wg != nullptr, job.big);
   cudaError_t e = ensure_max_smem((const void*)cluster_bond_kernel);
@@ -2806,7 +2844,27 @@ int max_active_clusters_query(int C, size_t smem) {
   cfg.numAttrs = 1;
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, cluster_bond_kernel, &cfg) != cudaSuccess) return 0;
-  return n;
+  // The occupancy calculator assumes one CTA per SM for kernels that
+  // allocate tensor memory (measured: tools/micro/tmem_occ.cu reports 1
+  // block/SM while the hardware keeps two 256-column CTAs resident).  Scale
+  // its answer by the residency the registers, shared memory, threads and
+  // TMEM columns (TW_NCOLS per CTA of 512) actually allow.
+  int api = 0, dev = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&api, cluster_bond_kernel, CT, smem) != cudaSuccess || api <= 0)
+    return n;
+  cudaFuncAttributes fa{};
+  int regs_sm = 0, smem_sm = 0, thr_sm = 0, resv = 0;
+  cudaGetDevice(&dev);
+  cudaFuncGetAttributes(&fa, (const void*)cluster_bond_kernel);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+  cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+  int bps = std::min(thr_sm / CT, regs_sm / std::max(1, regs_warp * CW));
+  bps = std::min(bps, (int)(smem_sm / std::max<size_t>(1, smem + fa.sharedSizeBytes + resv)));
+  bps = std::min(bps, 512 / TW_NCOLS);
+  return bps > api ? n * bps / api : n;
 }
 
 #ifdef TTP_DEV
@@ -2826,6 +2884,16 @@ int debug_phase_clocks(int enable, int64_t* out, int32_t n) {
     if (cudaMemcpyToSymbol(g_phase_clock, z, sizeof(z)) != cudaSuccess) return TTP_ERR_CUDA;
   }
   if (cudaMemcpyToSymbol(g_phase_enable, &en, sizeof(int)) != cudaSuccess) return TTP_ERR_CUDA;
+  return TTP_OK;
+}
+
+// Per-instance [start, end, sm] of the last enabled launches (n instances).
+int debug_inst_times(int64_t* out, int32_t n) {
+  n = std::min(n, INST_T_MAX);
+  for (int k = 0; k < 3; ++k)
+    if (cudaMemcpyFromSymbol(out + (size_t)k * n, g_inst_t, sizeof(long long) * n, sizeof(long long) * k * INST_T_MAX) !=
+        cudaSuccess)
+      return TTP_ERR_CUDA;
   return TTP_OK;
 }
 

@@ -82,9 +82,10 @@ def test_dev_knob_is_bitwise_neutral(tmp_path, release, knobs):
 def test_throughput_and_latency_instantiations_agree(tmp_path):
     """The 256-thread two-CTAs-per-SM instantiation (shipped for r <= 32) and
     the 512-thread one (shipped for r = 64) give the same cores when the
-    column basis runs separate partials passes (TTP_FUSED_QR=0; the fused
-    pass sums its dot products per warp, so its rounding follows the CTA
-    width)."""
-    tp = _run(tmp_path, "tp", {"TTP_DEV_LIBRARY": "1", "TTP_CK": "tp", "TTP_FUSED_QR": "0"})
-    lat = _run(tmp_path, "lat", {"TTP_DEV_LIBRARY": "1", "TTP_CK": "lat", "TTP_FUSED_QR": "0"})
+    column basis is the restated zlaqp2 with separate partials passes
+    (TTP_TSQR=0, TTP_FUSED_QR=0): the TSQR splits rows per warp and the fused
+    pass sums its dot products per warp, so both round by the CTA width."""
+    knobs = {"TTP_DEV_LIBRARY": "1", "TTP_FUSED_QR": "0", "TTP_TSQR": "0"}
+    tp = _run(tmp_path, "tp", dict(knobs, TTP_CK="tp"))
+    lat = _run(tmp_path, "lat", dict(knobs, TTP_CK="lat"))
     _assert_same(tp, lat)
