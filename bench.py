@@ -40,6 +40,10 @@ import time
 
 import numpy as np
 
+# large chunked batches (cfg3) allocate and free tens of GB per step: let the
+# caching allocator grow segments instead of fragmenting them
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 UNIT = "options/s"

@@ -117,7 +117,7 @@ __device__ __forceinline__ Reflector tw_zlarfg(cplx alpha, double s2, double mx,
 // ---- one structured chunk step sequence (forward): [R; X] -> [R'; 0] with
 // R in TMEM (lane = column), X[i] = chunk row i of this lane's column.  On
 // return X holds the chunk's reflector vectors (column j = reflector j);
-// taus to tau_g[j].  vb: this warp's 2 x (TW_LC + 1) broadcast slots.
+// taus to tau_g[j].  vb: this warp's 2 x (TW_LC + 2) broadcast slots.
 // Steps j < j0 are skipped: the caller guarantees the chunk is zero in
 // columns < j0 (rows of a triangle), where every reflector is the identity
 // (tau = 0 exactly), so skipping them changes no bit.  Per step, the next
@@ -126,52 +126,63 @@ __device__ __forceinline__ Reflector tw_zlarfg(cplx alpha, double s2, double mx,
 __device__ __forceinline__ void tw_chunk_fwd(uint32_t ta, cplx (&X)[TW_LC], int r, cplx* vb, cplx* tau_g,
                                              int j0 = 0) {
   const int lane = threadIdx.x & 31;
+  // The owner lane publishes its raw column x and the reflector's scale
+  // (v = scal x); the others fold scal into their two scalars, and the owner
+  // scales its own column once at the end, so a step costs the owner a norm
+  // and zlarfg only.
+  cplx myscal = mk(1.0, 0.0);
   TmRow nx;
   if (j0 < r) tm_ld_async(ta, j0, nx);
   for (int j = j0; j < r; ++j) {
     cplx Rj = tm_wait_row(nx);
     if (j + 1 < r) tm_ld_async(ta, j + 1, nx);
-    cplx* b = vb + (j & 1) * (TW_LC + 1);
+    cplx* b = vb + (j & 1) * (TW_LC + 2);
     if (lane == j) {
-      double p[4] = {0.0, 0.0, 0.0, 0.0}, mx = 0.0;
+      double p[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int i = 0; i < TW_LC; ++i) {
         p[i & 3] = fma(X[i].x, X[i].x, fma(X[i].y, X[i].y, p[i & 3]));
-        mx = fmax(mx, fmax(fabs(X[i].x), fabs(X[i].y)));
-      }
-      const double s2 = (p[0] + p[1]) + (p[2] + p[3]);
-      Ssq ss = ssq_init();
-      if (!(mx > 1e-140 && mx < 1e140))
-#pragma unroll
-        for (int i = 0; i < TW_LC; ++i) ssq_addc(ss, X[i]);
-      const Reflector h = tw_zlarfg(Rj, s2, mx, ss);
-      const cplx scal = reflector_scale(h);
-#pragma unroll
-      for (int i = 0; i < TW_LC; ++i) {
-        X[i] = cmul(X[i], scal);
         b[i] = X[i];
       }
+      const double s2 = (p[0] + p[1]) + (p[2] + p[3]);
+      Reflector h;
+      if (s2 > 1e-280 && s2 < 1e280) {
+        h = zlarfg_fast(Rj, s2);
+      } else {  // tiny or huge column: the scaled LAPACK form
+        Ssq ss = ssq_init();
+#pragma unroll
+        for (int i = 0; i < TW_LC; ++i) ssq_addc(ss, X[i]);
+        h = zlarfg_core(Rj, ssq_norm(ss));
+      }
+      myscal = reflector_scale(h);
       b[TW_LC] = h.tau;
+      b[TW_LC + 1] = myscal;
       Rj = mk(h.beta, 0.0);
       tau_g[j] = h.tau;
     }
     __syncwarp();
     if (lane > j && lane < r) {
-      const cplx ct = cconj(b[TW_LC]);
-      cplx w0 = Rj, w1 = mk(0.0, 0.0);
+      // w = R(j,k) + v^H x_k = R(j,k) + conj(scal) (x^H x_k);  x_k -= (conj(tau) w scal) x
+      const cplx ct = cconj(b[TW_LC]), sc = b[TW_LC + 1];
+      cplx w0 = mk(0.0, 0.0), w1 = mk(0.0, 0.0);
 #pragma unroll
       for (int i = 0; i < TW_LC; i += 2) {
         w0 = cfmac(b[i], X[i], w0);
         w1 = cfmac(b[i + 1], X[i + 1], w1);
       }
-      const cplx tw = cmul(ct, cadd(w0, w1));
+      const cplx w = cfmac(sc, cadd(w0, w1), Rj);
+      const cplx tw = cmul(ct, w);
       Rj = csub(Rj, tw);
+      const cplx tws = cmul(tw, sc);
 #pragma unroll
-      for (int i = 0; i < TW_LC; ++i) X[i] = csub(X[i], cmul(tw, b[i]));
+      for (int i = 0; i < TW_LC; ++i) X[i] = csub(X[i], cmul(tws, b[i]));
     }
     __syncwarp();
     tm_st_async(ta, j, Rj);
   }
+  if (lane >= j0 && lane < r)
+#pragma unroll
+    for (int i = 0; i < TW_LC; ++i) X[i] = cmul(X[i], myscal);
   tm_wait_st();
 }
 
@@ -183,6 +194,7 @@ __device__ __forceinline__ void tw_chunk_fwd(uint32_t ta, cplx (&X)[TW_LC], int 
 __device__ __forceinline__ void tw_chunk_rev(uint32_t ta, cplx (&W)[TW_LC], int r, const cplx* V, long long ldv,
                                              int nrow, const cplx* tau_g, int j0 = 0) {
   const int lane = threadIdx.x & 31;
+  // the next reflector's values are loaded one step ahead (L1 hits)
   cplx vn[TW_LC];
   cplx tn;
   auto loadv = [&](int j) {
@@ -377,114 +389,121 @@ __device__ __forceinline__ double tw_tsum16(const double (&v)[16], Op op) {
   return op(k1, __shfl_xor_sync(0xffffffffu, k1, 1));
 }
 
-// zlaqp2 on the final r x r triangle (column-major, ld r, in shared memory),
-// warp 0, lane-owned columns (j = lane, lane + 32): the reference's pivot
-// rule (first maximum of the partial norms), reflectors, partial-norm
-// downdate and recompute test, restated as in column_basis (squared norms).
-// Then Z = H_0 ... H_{r-1} [I] (zung2r) into Z (column-major, ld r).
-__device__ void ts_qrcp_small(CC& c, cplx* R, cplx* Z, double rank_tol, int* singular) {
+// zlaqp2 + zung2r on the final r x r triangle (r <= 32), all warps of the
+// CTA: lane = row, warp w owns columns j = w (mod CW).  Every warp derives
+// the pivot (first maximum of the squared partial norms) and the reflector
+// itself from shared memory, identically, so a step needs two block
+// barriers.  The reference's rules (zgeqp3 -> zlaqp2): partial-norm downdate with the
+// tol3z recompute test on squared norms as in column_basis, the rank
+// check of _column_basis (cross.py:110-118).
+__device__ void ts_qrcp_block(CC& c, cplx* R, cplx* Z, double rank_tol, int* singular) {
   const int r = c.r;
-  const int lane = threadIdx.x & 31;
-  for (int j = lane; j < r; j += 32) {
-    const double n2 = ssq_norm2(ssq_of(R + (long long)j * r, 1, r));
-    c.cn1[j] = n2;
-    c.cn2[j] = n2;
-    c.colmap[j] = j;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < r; j += CW) {
+    Ssq sq = ssq_init();
+    if (lane < r) ssq_addc(sq, R[(long long)j * r + lane]);
+    sq = warp_ssq(sq);
+    if (lane == 0) {
+      const double n2 = ssq_norm2(sq);
+      c.cn1[j] = n2;
+      c.cn2[j] = n2;
+      c.colmap[j] = j;
+    }
   }
-  __syncwarp();
+  __syncthreads();
   for (int i = 0; i < r; ++i) {
     ArgMax am{-1.0, LLONG_MAX};
-    for (int j = i + lane; j < r; j += 32)
-      if (argmax_better(c.cn1[j], j, am.v, am.key)) am = ArgMax{c.cn1[j], j};
+    if (i + lane < r) am = ArgMax{c.cn1[i + lane], i + lane};
     am = warp_argmax(am);
     const int p = (int)am.key;
+    __syncthreads();  // every warp has read cn1
     if (p != i) {
-      for (int row = lane; row < r; row += 32) {
-        const cplx t = R[(long long)p * r + row];
-        R[(long long)p * r + row] = R[(long long)i * r + row];
-        R[(long long)i * r + row] = t;
+      if ((int)threadIdx.x < r) {
+        const int t = threadIdx.x;
+        const cplx a = R[(long long)p * r + t];
+        R[(long long)p * r + t] = R[(long long)i * r + t];
+        R[(long long)i * r + t] = a;
       }
-      if (lane == 0) {
+      if (threadIdx.x == 0) {
         const int t = c.colmap[p];
         c.colmap[p] = c.colmap[i];
         c.colmap[i] = t;
         c.cn1[p] = c.cn1[i];
         c.cn2[p] = c.cn2[i];
       }
+      __syncthreads();
     }
-    __syncwarp();
-    // reflector of column i, rows i..r-1
-    cplx* col = R + (long long)i * r;
-    const cplx alpha = col[i];
-    double s2 = 0.0, mx = 0.0;
-    for (int row = i + 1 + lane; row < r; row += 32) {
-      s2 = fma(col[row].x, col[row].x, fma(col[row].y, col[row].y, s2));
-      mx = fmax(mx, fmax(fabs(col[row].x), fabs(col[row].y)));
-    }
+    // reflector of column i (every warp, identically)
+    const cplx x = (lane < r) ? R[(long long)i * r + lane] : mk(0.0, 0.0);
+    const bool below = lane > i && lane < r;
+    double s2 = below ? cabs2(x) : 0.0, mx = below ? fmax(fabs(x.x), fabs(x.y)) : 0.0;
     s2 = warp_sum(s2);
     mx = warp_max(mx);
+    const cplx alpha = mk(__shfl_sync(0xffffffffu, x.x, i), __shfl_sync(0xffffffffu, x.y, i));
     Reflector h;
     if (mx > 1e-140 && mx < 1e140) {
       h = zlarfg_fast(alpha, s2);
     } else {
-      const Ssq ss = ssq_of(col + i + 1, 1, r - i - 1);
-      h = zlarfg_core(alpha, ssq_norm(ss));
+      Ssq sq = ssq_init();
+      if (below) ssq_addc(sq, x);
+      h = zlarfg_core(alpha, ssq_norm(warp_ssq(sq)));
     }
     const cplx scal = reflector_scale(h);
-    __syncwarp();
-    for (int row = i + 1 + lane; row < r; row += 32) col[row] = cmul(col[row], scal);
-    if (lane == 0) {
-      col[i] = mk(h.beta, 0.0);
-      c.tau[i] = h.tau;
-      c.betas[i] = fabs(h.beta);
-    }
-    __syncwarp();
-    // H^H to the trailing columns + partial-norm downdates (lane = column)
+    const cplx v = below ? cmul(x, scal) : mk(lane == i ? 1.0 : 0.0, 0.0);
     const cplx ct = cconj(h.tau);
-    for (int j = i + 1 + lane; j < r; j += 32) {
-      cplx* cj = R + (long long)j * r;
-      cplx w = cj[i];
-      for (int row = i + 1; row < r; ++row) w = cfmac(col[row], cj[row], w);
-      const cplx tw = cmul(ct, w);
-      cj[i] = csub(cj[i], tw);
-      for (int row = i + 1; row < r; ++row) cj[row] = csub(cj[row], cmul(tw, col[row]));
+    for (int j = i + 1 + ((warp - (i + 1)) % CW + CW) % CW; j < r; j += CW) {
+      cplx a = (lane < r) ? R[(long long)j * r + lane] : mk(0.0, 0.0);
+      const cplx w = warp_sum(lane >= i ? cmulc(v, a) : mk(0.0, 0.0));
+      if (lane >= i && lane < r) {
+        a = csub(a, cmul(cmul(ct, w), v));
+        R[(long long)j * r + lane] = a;
+      }
+      const cplx rij = mk(__shfl_sync(0xffffffffu, a.x, i), __shfl_sync(0xffffffffu, a.y, i));
       const double s1 = c.cn1[j];
       if (s1 != 0.0) {
-        const double s1n = fmax(s1 - cabs2(cj[i]), 0.0);
+        const double s1n = fmax(s1 - cabs2(rij), 0.0);
         if (s1n <= TOL3Z * c.cn2[j]) {
-          const double n2 = (i < r - 1) ? ssq_norm2(ssq_of(cj + i + 1, 1, r - i - 1)) : 0.0;
-          c.cn1[j] = n2;
-          c.cn2[j] = n2;
-        } else {
+          Ssq sq = ssq_init();
+          if (lane > i && lane < r) ssq_addc(sq, a);
+          const double n2 = (i < r - 1) ? ssq_norm2(warp_ssq(sq)) : 0.0;
+          if (lane == 0) {
+            c.cn1[j] = n2;
+            c.cn2[j] = n2;
+          }
+        } else if (lane == 0) {
           c.cn1[j] = s1n;
         }
       }
     }
-    __syncwarp();
+    if (warp == i % CW) {
+      if (below) R[(long long)i * r + lane] = v;
+      if (lane == i) R[(long long)i * r + i] = mk(h.beta, 0.0);
+      if (lane == 0) {
+        c.tau[i] = h.tau;
+        c.betas[i] = fabs(h.beta);
+      }
+    }
+    __syncthreads();
   }
-  // rank check of _column_basis (cross.py:110-118)
   double lead = 0.0, mn = INFINITY;
   for (int t = 0; t < r; ++t) {
     lead = fmax(lead, c.betas[t]);
     mn = fmin(mn, c.betas[t]);
   }
-  *singular = (lead == 0.0 || mn < rank_tol * lead) ? 1 : 0;
-  // Z = H_0 ... H_{r-1} [I]: lane-owned columns, reflectors applied from the last
-  for (int j = lane; j < r; j += 32)
-    for (int row = 0; row < r; ++row) Z[(long long)j * r + row] = mk(row == j ? 1.0 : 0.0, 0.0);
-  __syncwarp();
+  if (threadIdx.x == 0) *singular = (lead == 0.0 || mn < rank_tol * lead) ? 1 : 0;
+  // Z = H_0 ... H_{r-1} [I] (zung2r), columns over the warps
+  for (int j = warp; j < r; j += CW)
+    if (lane < r) Z[(long long)j * r + lane] = mk(lane == j ? 1.0 : 0.0, 0.0);
+  __syncthreads();
   for (int i = r - 1; i >= 0; --i) {
-    const cplx* col = R + (long long)i * r;
+    const cplx v = (lane > i && lane < r) ? R[(long long)i * r + lane] : mk(lane == i ? 1.0 : 0.0, 0.0);
     const cplx ti = c.tau[i];
-    for (int j = i + lane; j < r; j += 32) {
-      cplx* zj = Z + (long long)j * r;
-      cplx w = zj[i];
-      for (int row = i + 1; row < r; ++row) w = cfmac(col[row], zj[row], w);
-      const cplx tw = cmul(ti, w);
-      zj[i] = csub(zj[i], tw);
-      for (int row = i + 1; row < r; ++row) zj[row] = csub(zj[row], cmul(tw, col[row]));
+    for (int j = i + ((warp - i) % CW + CW) % CW; j < r; j += CW) {
+      cplx z = (lane < r) ? Z[(long long)j * r + lane] : mk(0.0, 0.0);
+      const cplx w = warp_sum(lane >= i ? cmulc(v, z) : mk(0.0, 0.0));
+      if (lane >= i && lane < r) Z[(long long)j * r + lane] = csub(z, cmul(cmul(ti, w), v));
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -515,9 +534,9 @@ __device__ __forceinline__ TwScratch tw_scratch(cplx* base, int ms, int r, int C
 
 // Whether the TSQR column basis applies to this launch (cluster-uniform).
 __device__ __forceinline__ bool tsqr_usable(const CC& c, const ClusterJob& J) {
-  // r in [17, 32]: lane = column, and the per-warp broadcast slots (2r
-  // complex of wrow) hold 2 x 17 entries
-  if (!c.ns_global || !J.Sg || !J.tsqr || c.r > 32 || c.r < 17) return false;
+  // r <= 32: lane = column; the per-warp broadcast slots (2r complex of
+  // wrow) must hold 2 x (TW_LC + 2) entries and the dense block's r + 1
+  if (!c.ns_global || !J.Sg || !J.tsqr || c.r > 32 || 2 * c.r < 2 * (TW_LC + 2)) return false;
   const int ms = c.ldw, last = c.m - (c.C - 1) * ms;
   // every warp's rows start with a dense r x r block
   const int rpw0 = (ms + CW - 1) / CW, rpw1 = (last + CW - 1) / CW;
@@ -675,7 +694,8 @@ __device__ bool tsqr_basis(cg::cluster_group& cl, CC& c, const ClusterJob& J, in
   // ---- 3. across the cluster into CTA 0, zlaqp2 on the final triangle, and
   //         back down to every CTA's warp 0
   cl.sync();
-  if (crank == 0 && warp == 0) {
+  if (crank == 0) {
+  if (warp == 0) {
     for (int p = 1; p < C; ++p) {
       const TwScratch Sp = tw_scratch(sbase + p * tstride, ms, r, C);
       for (int k = 0; k < ntc; ++k) {
@@ -685,14 +705,15 @@ __device__ bool tsqr_basis(cg::cluster_group& cl, CC& c, const ClusterJob& J, in
         tw_store_v(X, r, S.XV + ((long long)p * TW_TC + k) * TW_LC * r);
       }
     }
-    cplx* Rs = c.aug;
-    cplx* Zs = c.aug + rr;
-    tw_export(ta, r, Rs);
-    __syncwarp();
-    int sing = 0;
-    ts_qrcp_small(c, Rs, Zs, rank_tol, &sing);
-    if (lane == 0) *flag = sing;
-    __syncwarp();
+    tw_export(ta, r, c.aug);
+  }
+  __syncthreads();
+  SP_BEGIN(spx);
+  cplx* Rs = c.aug;
+  cplx* Zs = c.aug + rr;
+  ts_qrcp_block(c, Rs, Zs, rank_tol, flag);
+  SP(spx, 5);
+  if (warp == 0) {
     tw_import(ta, r, Zs);
     for (int p = C - 1; p >= 1; --p) {
       const TwScratch Sp = tw_scratch(sbase + p * tstride, ms, r, C);
@@ -709,6 +730,7 @@ __device__ bool tsqr_basis(cg::cluster_group& cl, CC& c, const ClusterJob& J, in
             if (i < nrow) Sp.Zx[(long long)lane * r + k * TW_LC + i] = W[i];
       }
     }
+  }
   }
   cl.sync();
   SP(spq, 2);

@@ -16,7 +16,8 @@ from paper_2203_02804_b200 import _lib, configs  # noqa: E402
 
 lib = _lib.load_library()
 names = ["load", "colbasis", "-", "start1", "start2", "swaps1", "swaps2", "final", "end"]
-for cid, nb in ((4, 1), (4, 148), (2, 1), (1, 1)):
+cases = [tuple(int(x) for x in c.split(":")) for c in os.environ.get("PT_CASES", "4:1,4:148,2:1,1:1").split(",")]
+for cid, nb in cases:
     spec = configs.CONFIGS[cid]
     models = [configs.make_model(cid, i) for i in range(nb)]
     shape = (spec.grid.points_per_axis,) * spec.d
