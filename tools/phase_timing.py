@@ -47,7 +47,8 @@ for cid, nb in cases:
     sub = ["pivot+recomp", "partials", "clsync", "reduce", "update", "wy.gram", "wy.exchange"]
     print("    colbasis sub-phases (all bonds of the sweep): " + " ".join(
         f"{sub[k]}={out[16 + k] / ghz / 1e3:.1f}us" for k in range(7))
-        + f" wy.T={out[16 + 14] / ghz / 1e3:.1f}us wy.M+sync={out[16 + 15] / ghz / 1e3:.1f}us", flush=True)
+        + f" wy.T={out[16 + 14] / ghz / 1e3:.1f}us wy.M+sync={out[16 + 15] / ghz / 1e3:.1f}us"
+        + f" | slot6={out[16 + 6] / ghz / 1e3:.1f}us slot7={out[16 + 7] / ghz / 1e3:.1f}us raw14={out[16 + 14]} raw15={out[16 + 15]}", flush=True)
     sub2 = ["sw.publish", "sw.clsync", "sw.winner", "sw.barrier", "sw.selb", "sw.rowpass"]
     print("    swap sub-phases (all bonds, both runs): " + " ".join(
         f"{sub2[k]}={out[24 + k] / ghz / 1e3:.1f}us" for k in range(6)), flush=True)
