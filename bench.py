@@ -345,6 +345,8 @@ def parity_check(cid, gpu_prices, cpu_prices):
            "band": f"{BAND_FACTOR} x the instance's reference noise band (tests/golden/noise_bands.json: the "
                    "reference's own price spread under 1e-15 oracle noise)",
            "max_band_ratio": max(ratios), "ok": bool(max(ratios) <= 1.0),
+           "worst": {"instance": rows[int(np.argmax(ratios))][0], "rel": rows[int(np.argmax(ratios))][1],
+                     "band": rows[int(np.argmax(ratios))][2] or cfg_band},
            "against": sorted({s for *_, s in rows})}
     if cpu_prices is not None and gold:
         same = [cpu_prices[i] == gold[f"cfg{cid}_i{i}"]["price"] for i in range(len(cpu_prices))

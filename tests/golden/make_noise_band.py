@@ -9,8 +9,8 @@ around the unperturbed one is how far the reference's own TT price moves under
 rounding-level changes of its inputs -- the yardstick for an independent
 implementation's end-to-end price.
 
-Usage: OPENBLAS_NUM_THREADS=1 python tests/golden/make_noise_band.py CID N_INST N_SEEDS
-(merges into noise_bands.json).
+Usage: OPENBLAS_NUM_THREADS=1 python tests/golden/make_noise_band.py CID N_INST N_SEEDS [FIRST]
+(instances FIRST .. N_INST-1, default FIRST = 0; merges into noise_bands.json).
 """
 import json
 import os
@@ -51,11 +51,12 @@ def run(job):
 
 if __name__ == "__main__":
     cid, n_inst, n_seeds = (int(a) for a in sys.argv[1:4])
-    jobs = [(cid, i, s) for i in range(n_inst) for s in [-1] + list(range(n_seeds))]
+    first = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    jobs = [(cid, i, s) for i in range(first, n_inst) for s in [-1] + list(range(n_seeds))]
     with ProcessPoolExecutor(max_workers=int(os.environ.get('BAND_WORKERS', os.cpu_count()))) as ex:
         res = dict(ex.map(run, jobs))
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
-    for i in range(n_inst):
+    for i in range(first, n_inst):
         base = res[(cid, i, -1)][0]
         rel = sorted(abs(res[(cid, i, s)][0] - base) / abs(base) for s in range(n_seeds))
         data[f"cfg{cid}_i{i}"] = {"unperturbed": base, "rel_dev_sorted": rel, "max": max(rel),

@@ -1,5 +1,5 @@
 """Where the e2e (public API, host inputs) step spends time beyond the
-device-resident step (dev tool)."""
+device-resident step (dev tool).  Usage: python tools/e2e_gap.py [CID] [N]"""
 import sys
 import time
 
@@ -10,11 +10,13 @@ import paper_2203_02804_b200 as P  # noqa: E402
 from paper_2203_02804_b200 import configs  # noqa: E402
 from paper_2203_02804_b200.pricers import price_fourier_tt_batch_capi, run_cross_pair  # noqa: E402
 
-sp = configs.CONFIGS[4]
+CID = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+NB = int(sys.argv[2]) if len(sys.argv) > 2 else 592
+sp = configs.CONFIGS[CID]
 grid = sp.grid
 shape = (grid.points_per_axis,) * grid.d
 cfg = P.CrossConfig(bond_dim=sp.bond_dim, seed=sp.cross_seed)
-models = [configs.make_model(4, i) for i in range(592)]
+models = [configs.make_model(CID, i) for i in range(NB)]
 phi_b = P.OracleBatch([P.PhiGridOracle(m, grid) for m in models])
 v_b = P.OracleBatch([P.PayoffGridOracle(m, grid, conj=True) for m in models])
 
