@@ -5,7 +5,10 @@
 #include "ttp_common.cuh"
 #include "ttp_internal.h"
 
-#define BOND_THREADS 512
+// one-CTA kernel: blocks of at most this many bytes run the 128-thread shape
+#ifndef V0_SMALL_BYTES
+#define V0_SMALL_BYTES (64 << 10)
+#endif
 
 struct BondJob {
   int m, r;               // tall block rows / cols (m >= r)
@@ -42,7 +45,7 @@ struct BondJob {
   int rr;                 // right count (right-to-left decode)
 };
 
-size_t bond_smem_bytes(int r);
+size_t bond_smem_bytes(int m, int r);
 cudaError_t launch_bond(const BondJob& job, int n_inst, cudaStream_t s);
 
 // Cluster variant (k_cluster.cu): one thread-block cluster per instance, the
