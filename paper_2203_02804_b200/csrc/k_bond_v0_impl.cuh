@@ -113,19 +113,35 @@ __device__ void load_aug_from_Q(const Ctx& c, const int* rows) {
   __syncthreads();
 }
 
+// Running argmax of |z| (numpy abs = hypot, first maximum) with a squared-
+// modulus screen: hypot is only evaluated when z2 = re^2 + im^2 comes within
+// rounding of the running best's.  Below that, hypot(z) < a.v strictly (both
+// are accurate to an ulp and the margin is ~50 ulp), so the (value, key)
+// winner is bitwise the unscreened one; ties and non-finite values take the
+// exact path.  a2: squared modulus of a's entry, -1 before the first.
+__device__ __forceinline__ void argmax_abs_update(cplx z, long long key, ArgMax& a, double& a2) {
+  const double z2 = fma(z.x, z.x, z.y * z.y);
+  if (z2 >= a2 * (1.0 - 1e-14)) {
+    const double v = cabsh(z);
+    if (argmax_better(v, key, a.v, a.key)) {
+      a = ArgMax{v, key};
+      a2 = z2;
+    }
+  }
+}
+
 // B = Q X with X = right half of aug; returns the block argmax of |B|
 // (key = row-major flat index, numpy argmax order).
 __device__ ArgMax form_B(const Ctx& c) {
   const int m = c.m, r = c.r, ld = 2 * r;
   ArgMax a{-1.0, LLONG_MAX};
+  double a2 = -1.0;
   for (int l = threadIdx.x; l < m; l += NT) {
     for (int j = 0; j < r; ++j) {
       cplx acc = mk(0.0, 0.0);
       for (int t = 0; t < r; ++t) acc = cfma(Qat(c, l, t), c.aug[t * ld + r + j], acc);
       Bat(c, l, j) = acc;
-      const double v = cabsh(acc);
-      const long long key = (long long)l * r + j;
-      if (argmax_better(v, key, a.v, a.key)) a = ArgMax{v, key};
+      argmax_abs_update(acc, (long long)l * r + j, a, a2);
     }
   }
   return block_argmax(a, c.red);
@@ -196,10 +212,12 @@ __device__ void column_basis(const Ctx& c) {
       cplx* cj = A + (long long)c.colmap[j] * m;
       cplx sacc = mk(0.0, 0.0);
       if (lane == 0) sacc = cj[i];  // v_i = 1
+#pragma unroll 4
       for (int l = i + 1 + lane; l < m; l += 32) sacc = cfmac(col[l], cj[l], sacc);
       sacc = warp_sum(sacc);
       const cplx t = cmul(tc, sacc);
       if (lane == 0) cj[i] = csub(cj[i], t);
+#pragma unroll 4
       for (int l = i + 1 + lane; l < m; l += 32) cj[l] = csub(cj[l], cmul(col[l], t));
       __syncwarp();
       // zlaqp2 partial column norm update
@@ -237,10 +255,12 @@ __device__ void column_basis(const Ctx& c) {
       cplx* cj = A + (long long)c.colmap[j] * m;
       cplx sacc = mk(0.0, 0.0);
       if (lane == 0) sacc = cj[i];
+#pragma unroll 4
       for (int l = i + 1 + lane; l < m; l += 32) sacc = cfmac(col[l], cj[l], sacc);
       sacc = warp_sum(sacc);
       const cplx t = cmul(ti, sacc);
       if (lane == 0) cj[i] = csub(cj[i], t);
+#pragma unroll 4
       for (int l = i + 1 + lane; l < m; l += 32) cj[l] = csub(cj[l], cmul(col[l], t));
     }
     __syncthreads();
@@ -409,14 +429,13 @@ __device__ int swap_to_dominance(const Ctx& c, double slack, long long limit) {
     for (int t = threadIdx.x; t < r; t += NT) c.vec[t] = csub(Bat(c, sj, t), Bat(c, i, t));
     __syncthreads();
     a = ArgMax{-1.0, LLONG_MAX};
+    double a2 = -1.0;
     for (int l = threadIdx.x; l < m; l += NT) {
       const cplx blj = Bat(c, l, j);
       for (int t = 0; t < r; ++t) {
         const cplx nv = cadd(Bat(c, l, t), cdiv(cmul(blj, c.vec[t]), pivot));
         Bat(c, l, t) = nv;
-        const double v = cabsh(nv);
-        const long long key = (long long)l * r + t;
-        if (argmax_better(v, key, a.v, a.key)) a = ArgMax{v, key};
+        argmax_abs_update(nv, (long long)l * r + t, a, a2);
       }
     }
     __syncthreads();
