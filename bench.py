@@ -496,6 +496,7 @@ def main():
     value = n_total * args.steps / elapsed
     ok = int((rp.status == 0).sum() + (rv.status == 0).sum())
     gpu_prices_head = [float(x) for x in prices[:16]]
+    gpu_prices_all = np.array(prices, dtype=np.float64)
 
     # e2e through the public API with host inputs (sharded batch API at N > 1)
     e2e = None
@@ -610,6 +611,22 @@ def main():
         mean_sweeps = (np.mean(sw_phi) + np.mean(sw_v)) if sw_phi else None
         cpu_baseline, cpu_prices = cpu_baseline_sample(cid, cores, args.cpu_sample, sweeps_per_option=mean_sweeps)
     parity = parity_check(cid, gpu_prices_head, cpu_prices[:16] if cpu_prices else None)
+    if parity is not None and cpu_prices and len(cpu_prices) > 16:
+        # --cpu-sample N > 16: every one of the first N options of the timed
+        # batch against the pinned port's price (bitwise the reference's where
+        # goldens exist), judged against the widest per-instance band of the
+        # config since only instances 0-15 have bands of their own
+        nall = min(len(cpu_prices), len(gpu_prices_all))
+        cpu_all = np.array(cpu_prices[:nall])
+        rel = np.abs(gpu_prices_all[:nall] - cpu_all) / np.abs(cpu_all)
+        _, bands_all = _parity_goldens()
+        wide = max((v["max"] for k, v in bands_all.items() if isinstance(v, dict) and k.startswith(f"cfg{cid}_")),
+                   default=float("nan"))
+        parity["whole_sample_vs_port"] = {
+            "n": int(nall), "median_rel": float(np.median(rel)), "p90_rel": float(np.quantile(rel, 0.9)),
+            "max_rel": float(rel.max()), "worst_instance": int(np.argmax(rel)),
+            "widest_instance_band": wide, "n_above_widest_band": int((rel > wide).sum()),
+            "n_above_twice_widest_band": int((rel > BAND_FACTOR * wide).sum())}
     if parity is not None and grid.n_terms <= 2_000_000_000:
         # where the full-grid sum is feasible (configs 1-3): the same prices
         # and the reference's, both against the device dense sum (K8, equal to
