@@ -178,6 +178,21 @@ def test_p3_maxvol_property_suite():
             assert got >= best / 1.01 ** r - 1e-12
 
 
+def test_p3_maxvol_both_one_cta_shapes_against_the_oracle():
+    """The one-CTA bond kernel runs 128-thread CTAs for blocks of at most
+    64 KB and 512-thread CTAs above (csrc/k_bond_v0.cu).  Well-conditioned
+    matrices on both sides of the boundary, and at the 1 MB boundary to the
+    cluster kernel, select the rows the pinned oracle (= the reference's
+    maxvol, cross.py:208-230) selects."""
+    rng = np.random.default_rng(64)
+    # (rows, cols): bytes = rows * cols * 16
+    for n, r in [(200, 16), (255, 16), (257, 16), (300, 16), (129, 32), (1300, 20), (2047, 32), (2049, 32)]:
+        m = rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r))
+        rows = P.maxvol(m, slack=0.01)
+        np.testing.assert_array_equal(rows, O.maxvol(m, slack=0.01), err_msg=f"{n} x {r}")
+        assert np.abs(m @ np.linalg.inv(m[rows])).max() <= 1.01 + 1e-9
+
+
 def test_p3_maxvol_edge_cases():
     np.testing.assert_array_equal(P.maxvol(np.array([[1.0], [10.0], [3.0]])), [1])
     sq = np.random.default_rng(0).standard_normal((4, 4)) + 0j
