@@ -601,7 +601,14 @@ __device__ __forceinline__ double cd_bfrag(const cplx* G, int ra, int rb, int k0
 //   CD_TAB2   site 2 from that table: row i_1(j) * n0 + i_0(j) of Vin
 constexpr int CD_PLAIN = 0, CD_G0 = 1, CD_TAB1 = 2, CD_TAB2 = 3;
 
-template <int NT, int KS, int MODE>
+// WC: warp columns (4, 2 or 1) of the 8 warps; 8 / WC warp rows of
+// CD_ROWS / (8 * 8 / WC) m-tiles each.  N' = 2 rb is covered by WC * NT
+// 8-wide n-tiles: 4 x {1, 2, 4} wastes up to 37% of the MMAs on bonds that
+// are not multiples of 16 (rb = 20: 64 columns for 40), so rb = 17..24
+// takes 2 x 3 (48 columns; configs 2/3: conv site 4.16 -> 3.68 ms per
+// launch).  Every output entry keeps its k order, so the variants are
+// bitwise equal.
+template <int NT, int KS, int MODE, int WC>
 __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
     const cplx* __restrict__ cores, long long stride, long long offk, int ra, int n, int rb,
     const int* __restrict__ perm, const int* __restrict__ goff, const cplx* __restrict__ Vin,
@@ -680,7 +687,9 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int wr = warp & 1, wc = warp >> 1;
+  constexpr int WR = 8 / WC, MT = CD_ROWS / (8 * WR);
+  static_assert(WC == 1 || WC == 2 || WC == 4, "8 warps as WR x WC");
+  const int wr = warp % WR, wc = warp / WR;
   const int ncol0 = wc * NT * 8;  // first real column (of N') of this warp
   double breg[KS > 0 ? KS : 1][NT];
   if constexpr (KS > 0) {
@@ -702,26 +711,26 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
     __syncthreads();
     const double* st = buf ? stage1 : stage0;
     const int* rj = rowj + buf * CD_ROWS;
-    double acc[CD_MT][NT][2];
+    double acc[MT][NT][2];
 #pragma unroll
-    for (int mt = 0; mt < CD_MT; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    const double* arow = st + (wr * 8 * CD_MT + gid) * KP + tig;
+    const double* arow = st + (wr * 8 * MT + gid) * KP + tig;
     // the table's buckets are n0 = N+1 rows (odd): warps whose rows of the
     // last tile are all past it skip their MMAs (table mode only)
     bool skip_mma = false;
-    if constexpr (MODE == CD_TAB1) skip_mma = g0 + tile * CD_ROWS + wr * 8 * CD_MT >= g1;
+    if constexpr (MODE == CD_TAB1) skip_mma = g0 + tile * CD_ROWS + wr * 8 * MT >= g1;
     if constexpr (KS > 0) {
       if (!skip_mma)
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         if (4 * ks >= Kpad) break;  // KS rounds the k-steps up; columns past Kpad are not staged
-        double av[CD_MT];
+        double av[MT];
 #pragma unroll
-        for (int mt = 0; mt < CD_MT; ++mt) av[mt] = arow[mt * 8 * KP + 4 * ks];
+        for (int mt = 0; mt < MT; ++mt) av[mt] = arow[mt * 8 * KP + 4 * ks];
 #pragma unroll
-        for (int mt = 0; mt < CD_MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -729,13 +738,13 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
       }
     } else {
       for (int k0 = 0; k0 < Kpad; k0 += 4) {
-        double av[CD_MT], bv[NT];
+        double av[MT], bv[NT];
 #pragma unroll
-        for (int mt = 0; mt < CD_MT; ++mt) av[mt] = arow[mt * 8 * KP + k0];
+        for (int mt = 0; mt < MT; ++mt) av[mt] = arow[mt * 8 * KP + k0];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) bv[nt] = cd_bfrag(G, ra, rb, k0, ncol0 + nt * 8, gid, tig);
 #pragma unroll
-        for (int mt = 0; mt < CD_MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -747,8 +756,8 @@ __global__ void __launch_bounds__(CD_THREADS, 2) conv_site_dmma_kernel(
     }
     // c0, c1 = C'[row][2 tig], C'[row][2 tig + 1] = one complex output
 #pragma unroll
-    for (int mt = 0; mt < CD_MT; ++mt) {
-      const int j = rj[wr * 8 * CD_MT + mt * 8 + gid];
+    for (int mt = 0; mt < MT; ++mt) {
+      const int j = rj[wr * 8 * MT + mt * 8 + gid];
       if (j < 0) continue;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
@@ -775,31 +784,36 @@ cudaError_t launch_conv_site_dmma(const cplx* cores, long long stride, long long
                                   int rb, const int* perm, const int* goff, const cplx* vin, cplx* vout,
                                   long long vstride, const int* active, int n_inst, cudaStream_t s,
                                   long long off0, const int* idx0, int idx_d, int mode, int n0) {
-  const int nt = conv_site_dmma_nt(rb);
   const size_t smem = conv_site_dmma_smem(ra, rb);
   dim3 grid((unsigned)n, (unsigned)n_inst);
+  // warp layout: the fewest 8-wide n-tiles that cover N' = 2 rb
+  const int tiles = (2 * rb + 7) / 8;
+  int wc = 4, nt = conv_site_dmma_nt(rb);
+  if (tiles == 5 || tiles == 6) { wc = 2; nt = 3; }  // rb = 17..24 (1 x 3 for rb = 9..12 measured no gain)
   // register-resident B' when its KS x NT fragments fit in 32 registers
   const int ks_need = ((2 * ra + 3) & ~3) / 4;
-  const int ks = ks_need <= 4 ? 4 : ks_need <= 8 ? 8 : ks_need <= 16 ? 16 : 0;
-  const int code = nt * 100 + ((ks > 0 && ks * nt <= 32) ? ks : 0);
-#define CD_LAUNCH(NT, KS, MODE)                                                                  \
+  int ks = ks_need <= 4 ? 4 : ks_need <= 8 ? 8 : (ks_need <= 10 && wc == 2) ? 10 : ks_need <= 16 ? 16 : 0;
+  if (ks * nt > 32) ks = 0;
+  const int code = wc * 10000 + nt * 100 + ks;
+#define CD_LAUNCH(NT, KS, MODE, WC)                                                              \
   {                                                                                              \
-    cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS, MODE>);           \
+    cudaError_t e = ensure_max_smem((const void*)conv_site_dmma_kernel<NT, KS, MODE, WC>);       \
     if (e != cudaSuccess) return e;                                                              \
-    conv_site_dmma_kernel<NT, KS, MODE><<<grid, CD_THREADS, smem, s>>>(                          \
+    conv_site_dmma_kernel<NT, KS, MODE, WC><<<grid, CD_THREADS, smem, s>>>(                      \
         cores, stride, offk, ra, n, rb, perm, goff, vin, vout, vstride, active, off0, idx0, idx_d, n0); \
   }
-#define CD_CASE(NT, KS)                                                                          \
-  case NT * 100 + KS:                                                                            \
-    if (mode == CD_G0) CD_LAUNCH(NT, KS, CD_G0)                                                  \
-    else if (mode == CD_TAB1) CD_LAUNCH(NT, KS, CD_TAB1)                                         \
-    else if (mode == CD_TAB2) CD_LAUNCH(NT, KS, CD_TAB2)                                         \
-    else CD_LAUNCH(NT, KS, CD_PLAIN)                                                             \
+#define CD_CASE(WC, NT, KS)                                                                      \
+  case WC * 10000 + NT * 100 + KS:                                                               \
+    if (mode == CD_G0) CD_LAUNCH(NT, KS, CD_G0, WC)                                              \
+    else if (mode == CD_TAB1) CD_LAUNCH(NT, KS, CD_TAB1, WC)                                     \
+    else if (mode == CD_TAB2) CD_LAUNCH(NT, KS, CD_TAB2, WC)                                     \
+    else CD_LAUNCH(NT, KS, CD_PLAIN, WC)                                                         \
     break;
   switch (code) {
-    CD_CASE(1, 0) CD_CASE(1, 4) CD_CASE(1, 8) CD_CASE(1, 16)
-    CD_CASE(2, 0) CD_CASE(2, 4) CD_CASE(2, 8) CD_CASE(2, 16)
-    CD_CASE(4, 0) CD_CASE(4, 4) CD_CASE(4, 8)
+    CD_CASE(4, 1, 0) CD_CASE(4, 1, 4) CD_CASE(4, 1, 8) CD_CASE(4, 1, 16)
+    CD_CASE(4, 2, 0) CD_CASE(4, 2, 4) CD_CASE(4, 2, 8) CD_CASE(4, 2, 16)
+    CD_CASE(4, 4, 0) CD_CASE(4, 4, 4) CD_CASE(4, 4, 8)
+    CD_CASE(2, 3, 0) CD_CASE(2, 3, 4) CD_CASE(2, 3, 8) CD_CASE(2, 3, 10)
     default:
       return cudaErrorInvalidValue;
   }
