@@ -270,6 +270,11 @@ def max_batch(shape, cfg_phi, cfg_v, n=None, fraction=0.6):
     if n is not None and n * per <= _DEVICE_TOTAL[dev] // 3:
         return n
     free, _ = torch.cuda.mem_get_info()
+    # blocks torch's caching allocator holds but has not handed out are as good
+    # as free (it reuses them, and releases them before giving up on a request):
+    # without them a second call in the same process sees a fraction of the
+    # memory the first saw and runs the same batch in many more chunks
+    free += max(0, torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev))
     return max(1, int(fraction * free) // max(1, per))
 
 
