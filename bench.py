@@ -419,7 +419,7 @@ def main():
     import paper_2203_02804_b200 as P
     from paper_2203_02804_b200 import _lib, configs
     from paper_2203_02804_b200.distributed import gather_records, shard_range
-    from paper_2203_02804_b200.pricers import run_cross_pair
+    from paper_2203_02804_b200.pricers import balanced_chunk, run_cross_pair
 
     cid = args.config
     sp = spec_of(cid)
@@ -436,7 +436,7 @@ def main():
     # device-resident inputs for the `value` path, in chunks that fit device
     # memory (cfg3's 4096 instances; the public API chunks the same way)
     from paper_2203_02804_b200.pricers import max_batch
-    chunk = max_batch(shape, cfg, cfg, n=B)
+    chunk = balanced_chunk(B, max_batch(shape, cfg, cfg, n=B))
     chunks = []
     for c0 in range(0, B, chunk):
         ms = models[c0:c0 + chunk]

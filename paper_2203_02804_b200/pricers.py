@@ -278,6 +278,15 @@ def max_batch(shape, cfg_phi, cfg_v, n=None, fraction=0.6):
     return max(1, int(fraction * free) // max(1, per))
 
 
+def balanced_chunk(n, limit):
+    """Chunk size for n instances when at most `limit` fit at once: the fewest
+    chunks, of equal size (148 options with room for 122 run as 74 + 74, not
+    122 + 26: a short last chunk costs a full chunk's latency)."""
+    limit = max(1, int(limit))
+    k = -(-n // limit)
+    return -(-n // k) if k > 0 else limit
+
+
 def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference="never",
                            term_cap=DENSE_TERM_CAP, raise_errors=True, group=None):
     """Price many independent options on one grid with the device TT path.
@@ -307,7 +316,7 @@ def price_fourier_tt_batch(models, grid, cfg_phi, cfg_v, t=0.0, dense_reference=
     shape = (grid.points_per_axis,) * grid.d
     # memory-aware batching: instances that do not fit one launch pair run in
     # consecutive chunks (results identical: instances are independent)
-    chunk = max_batch(shape, cfg_phi, cfg_v, n=len(models))
+    chunk = balanced_chunk(len(models), max_batch(shape, cfg_phi, cfg_v, n=len(models)))
     if len(models) > chunk:
         out = []
         for i0 in range(0, len(models), chunk):

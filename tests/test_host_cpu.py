@@ -200,3 +200,19 @@ def test_tensor_train_container_rules():
     assert tt.bond_dims == (1, 2, 1) and tt.n_entries == 12
     with pytest.raises(ValueError):
         tt.cores[0][0, 0, 0] = 1.0
+
+
+def test_balanced_chunks_are_equal_and_fit():
+    """The batch API's chunking: the fewest chunks that respect the memory
+    limit, of equal size (never a short last chunk)."""
+    from paper_2203_02804_b200.pricers import balanced_chunk
+    assert balanced_chunk(148, 122) == 74          # config 5 on one B200: 74 + 74, not 122 + 26
+    assert balanced_chunk(4096, 1585) == 1366      # config 3: three equal chunks
+    assert balanced_chunk(592, 592) == 592 and balanced_chunk(592, 5000) == 592
+    assert balanced_chunk(5, 1) == 1 and balanced_chunk(1, 10) == 1
+    for n in (1, 7, 100, 1023, 4096):
+        for limit in (1, 3, 64, 999, 5000):
+            c = balanced_chunk(n, limit)
+            k = -(-n // c)
+            assert 1 <= c <= max(limit, 1) and k == -(-n // min(limit, n))
+            assert k * c - n < k                   # chunk sizes differ by at most one
